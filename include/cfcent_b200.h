@@ -1,0 +1,180 @@
+/*
+ * cfcent_b200 -- C-ABI of the B200-native multi-RHS Laplacian multigrid path.
+ *
+ * The reference (cfcent 0.1.0, pure Python) has no FFI; its boundary is the
+ * Python API of pkg/src/cfcent.  Each entry point below
+ * replaces one reference call site and is bound from the Python mirror
+ * (paper_1607_02955_b200/_native.py) with ctypes; INTEGRATION.md shows the
+ * binding a maintainer of the reference would add.
+ *
+ * Conventions
+ *  - plain pointers and sizes only; no torch / numpy types.
+ *  - host pointers unless the name ends in _dev.
+ *  - row-major blocks: a block of k right-hand sides over n nodes stored as
+ *    X[i * k + j] (node i, column j) is called "n x k row-major".
+ *  - "rows" layout (the reference's supplies / PotentialVector layout): one
+ *    right-hand side per row, S[r * n + i].
+ *  - every function returns a status: CF_OK, CF_DOMAIN (maps to DomainError),
+ *    CF_CONVERGENCE (maps to ConvergenceError, *best_residual filled),
+ *    CF_RUNTIME (CUDA / allocation failure).  cf_last_error() gives the message
+ *    of the last failure on the calling thread.
+ *  - handles are re-entrant: concurrent calls on one hierarchy serialise on a
+ *    per-handle lock (reference contract SPEC.md:196).
+ */
+#ifndef CFCENT_B200_H
+#define CFCENT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { CF_OK = 0, CF_DOMAIN = 1, CF_CONVERGENCE = 2, CF_RUNTIME = 3 };
+enum { CF_LEVEL_ELIMINATION = 0, CF_LEVEL_AGGREGATION = 1, CF_LEVEL_COARSEST = 2 };
+
+/* One hierarchy level in host memory (copied to the device by
+ * cf_hier_create).  Replaces solver.py:97-120 `Level`.
+ * Matrix: off-diagonal CSR (int32 column, fp64 value = L_ij < 0) plus the
+ * diagonal split out; required for level 0 and aggregation levels. */
+typedef struct {
+    int32_t kind;            /* CF_LEVEL_* */
+    int32_t n;               /* rows at this level */
+    int32_t n_coarse;        /* rows at the next level (0 for coarsest) */
+    int64_t nnz_off;         /* off-diagonal entries (0 if no matrix) */
+    const int64_t* rowptr;   /* n+1, offsets into col/val (NULL if no matrix) */
+    const int32_t* col;
+    const double* val;
+    const double* diag;      /* n */
+    /* aggregation (solver.py:110-114): colouring and aggregate map */
+    int32_t n_colors;
+    const int32_t* color_ptr;    /* n_colors+1 */
+    const int32_t* color_rows;   /* n, rows grouped by colour, ascending */
+    const int32_t* agg;          /* n, node -> aggregate */
+    const int32_t* agg_ptr;      /* n_coarse+1 */
+    const int32_t* agg_members;  /* n, members of each aggregate ascending */
+    /* elimination (solver.py:104-108) */
+    int32_t n_f;
+    const int32_t* f_nodes;      /* n_f */
+    const int32_t* c_nodes;      /* n_coarse */
+    const double* f_degree;      /* n_f */
+    const int64_t* wcf_ptr;      /* n_coarse+1; W_cf columns index f_nodes */
+    const int32_t* wcf_col;
+    const double* wcf_val;
+    const int64_t* wfc_ptr;      /* n_f+1; W_fc = W_cf^T, columns index c_nodes */
+    const int32_t* wfc_col;
+    const double* wfc_val;
+    /* coarsest (solver.py:115-116, 394-419): dense n x n operator
+     * M = (I - 11^T/n) G^+ with G^+ the node-0-grounded inverse padded by a
+     * zero row/column, so x = M b is the reference's direct solve. */
+    const double* coarse_op;
+} CfLevelDesc;
+
+/* Solve parameters (SolverConfig, solver.py:61-74, plus module constants
+ * solver.py:53-58). */
+typedef struct {
+    double tau;
+    int32_t max_cycles;
+    int32_t nu1, nu2;            /* smoothing_steps */
+    int32_t fcg_max_iters;       /* FCG_MAX_ITERS = 200 */
+    int32_t jpcg_max_iters;      /* max(2000, 50 sqrt(n)) */
+    double stop_margin;          /* STOP_MARGIN = 0.9 */
+    double stagnation_factor;    /* 0.9 */
+    int32_t stagnation_cycles;   /* 5 */
+} CfSolveParams;
+
+/* Per-call statistics (SolveStats, solver.py:123-137). */
+typedef struct {
+    int64_t solves;              /* columns solved (nonzero and zero) */
+    int64_t fallback_solves;     /* columns that entered FCG */
+    int64_t vcycles;             /* V-cycle column-applications executed */
+    int64_t outer_iterations;    /* block iterations executed */
+    double max_residual;
+    double best_residual;        /* on CF_CONVERGENCE: worst failing residual */
+} CfSolveStats;
+
+const char* cf_last_error(void);
+int cf_device_count(void);
+int cf_version(void);
+
+/* --- hierarchy (replaces solver.py:422-523 `setup` output upload) ------ */
+int cf_hier_create(int32_t n_levels, const CfLevelDesc* levels, int32_t device,
+                   void** out_handle);
+int cf_hier_destroy(void* handle);
+/* total device bytes owned by the hierarchy (operators + workspace) */
+int64_t cf_hier_device_bytes(void* handle);
+
+/* --- solves ------------------------------------------------------------- */
+/* solver.py:771-811 `solve_many` (and :754 `solve` with count = 1):
+ * supplies_rows (count x n, host) -> values_rows (count x n, host, centred)
+ * and residuals (count).  Columns are processed in device chunks of up to
+ * max_chunk columns; results never depend on chunking. */
+int cf_solve_rows(void* handle, const double* supplies_rows, int64_t count,
+                  const CfSolveParams* params, double* values_rows,
+                  double* residuals, CfSolveStats* stats);
+
+/* Same on device memory: B_dev, X_dev are n x k row-major (k <= 256). */
+int cf_solve_block_dev(void* handle, const double* B_dev, double* X_dev, int32_t k,
+                       const CfSolveParams* params, double* residuals,
+                       CfSolveStats* stats);
+
+/* Exported for unit tests: R = B - L X and per-column sum(R^2) on level 0
+ * (solver.py:694-695). Device pointers, n x k row-major. */
+int cf_residual_dev(void* handle, const double* B_dev, const double* X_dev, double* R_dev,
+                    int32_t k, double* colsq_host);
+
+/* --- estimators (resistance.py / centrality.py) ----------------------- */
+/* Graph upload for the JL right-hand sides: adjacency (graph.py:30-98) with
+ * per-entry canonical edge id (graph.py:78-86) and sqrt(w) per edge. */
+int cf_graph_create(void* hier, int64_t n, int64_t m, const int64_t* adj_ptr,
+                    const int32_t* adj_nbr, const int32_t* adj_edge,
+                    const double* sqrt_w, void** out_graph);
+int cf_graph_destroy(void* graph);
+
+/* resistance.py:181-199: rows [row0, row0+k) of Q W^1/2 B for
+ * Q = (default_rng(seed).integers(0,2,(K,m))*2-1)/sqrt(K), from the PCG64
+ * state (state_hi/lo, inc_hi/lo) of a fresh default_rng(seed).
+ * Output Y_rows (k x n host, UNcentred, bit-identical to the reference). */
+int cf_jl_rhs_rows(void* graph, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                   uint64_t inc_lo, int64_t K, int64_t row0, int32_t k,
+                   double* Y_rows);
+
+/* Fused JL estimator (build_sketch + sketch_distance_sums,
+ * resistance.py:161-237, centrality.py:140-166): generates Q on device,
+ * forms and centres Y, solves, and reduces Z without downloading it.
+ * out_sums[q] = sum_w ||z_v - z_w||^2 for query v = query[q].
+ * If z_rows is not NULL, also returns Z (K x n host, the sketch's z). */
+int cf_jl_sketch(void* graph, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                 uint64_t inc_lo, int64_t K, double inv_sqrt_k, const int64_t* query,
+                 int64_t n_query, const CfSolveParams* params, double* out_sums,
+                 double* z_rows, double* residuals, CfSolveStats* stats);
+
+/* Amortised node solutions L z_x = e_x - 1/n (resistance.py:77-99) for the
+ * given nodes, reduced on device to the |nodes| x |nodes| submatrix
+ * sub[a * cnt + b] = z_{nodes[a]}[nodes[b]] (what resistances_from_node and
+ * the sampling estimator read, resistance.py:124-129).  If z_rows is not
+ * NULL the full solutions (cnt x n) are returned too. */
+int cf_node_solutions(void* handle, const int64_t* nodes, int64_t cnt,
+                      const CfSolveParams* params, double* sub, double* z_rows,
+                      double* residuals, CfSolveStats* stats);
+
+/* --- host setup helpers (solver.py greedy loops) ---------------------- */
+/* solver.py:236-247: greedy ascending-id independent set of off-degree
+ * <= cap; writes chosen ids to out_f, returns the count in *n_f. */
+int cf_setup_elim_select(int64_t n, const int64_t* indptr, const int64_t* indices,
+                         int32_t cap, int64_t* out_f, int64_t* n_f);
+/* solver.py:297-346: seeds + affinity attachment, aggregate map in out_agg. */
+int cf_setup_aggregate(int64_t n, const int64_t* indptr, const int64_t* indices,
+                       const double* tv, int32_t n_tv, int64_t* out_agg, int64_t* n_agg);
+/* solver.py:364-380: greedy matching over a pre-sorted edge order. */
+int cf_setup_matching(int64_t n, int64_t n_edges, const int64_t* eu, const int64_t* ev,
+                      const int64_t* order, int64_t* out_agg, int64_t* n_agg);
+/* greedy natural-order colouring of the off-diagonal graph (multicolour
+ * Gauss-Seidel, the B200 smoother ordering). */
+int cf_setup_colour(int64_t n, const int64_t* indptr, const int64_t* indices,
+                    int32_t* out_colour, int32_t* n_colors);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CFCENT_B200_H */

@@ -1,0 +1,87 @@
+// Device-resident multigrid hierarchy and the batched solve driver (internal).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "cfcent_b200.h"
+
+namespace cf {
+
+struct DLevel {
+    int kind = 0, n = 0, nc = 0, nf = 0, ncolors = 0;
+    int64_t nnz = 0;
+    int64_t* rp = nullptr;
+    int32_t* col = nullptr;
+    double* val = nullptr;
+    double* diag = nullptr;
+    std::vector<int32_t> cptr;  // host copy of colour offsets
+    int32_t* crows = nullptr;
+    int32_t *agg = nullptr, *aptr = nullptr, *amem = nullptr;
+    int32_t *fn = nullptr, *cn = nullptr;
+    double* fd = nullptr;
+    int64_t* wcp = nullptr;
+    int32_t* wcc = nullptr;
+    double* wcv = nullptr;
+    int64_t* wfp = nullptr;
+    int32_t* wfc = nullptr;
+    double* wfv = nullptr;
+    double* M = nullptr;
+    // workspace, n x kc_ws row-major (level 0 uses Hier::R / Hier::C)
+    double* b = nullptr;
+    double* x = nullptr;
+    double* ls = nullptr;  // 2 x 256 line-search sums
+};
+
+// Supported block widths (columns per device chunk).
+constexpr int kMaxKC = 256;
+int pick_kc(int64_t remaining);
+
+struct Hier {
+    int dev = 0;
+    cudaStream_t s = nullptr;
+    std::vector<DLevel> L;
+    std::mutex mu;
+    int kc_ws = 0;  // workspace width currently allocated
+    int n0 = 0;
+    // level-0 block buffers, n0 x kc_ws
+    double *B = nullptr, *X = nullptr, *R = nullptr, *C = nullptr;
+    // fallback buffers (lazily allocated)
+    double *Z = nullptr, *P = nullptr, *AP = nullptr;
+    int kc_fb = 0;
+    double* parts = nullptr;
+    size_t parts_cap = 0;  // doubles
+    double* sums = nullptr;  // 8 x kMaxKC
+    double* coef = nullptr;  // 4 x kMaxKC
+    double *bn = nullptr, *res = nullptr, *prev = nullptr;
+    int *stall = nullptr, *state = nullptr, *count = nullptr;
+    int* h_count = nullptr;     // pinned
+    double* h_small = nullptr;  // pinned, 16 x kMaxKC
+    double* S = nullptr;        // staging for rows layout (kc_ws x n0)
+    std::vector<void*> owned;   // operator allocations
+    int64_t bytes = 0;
+    std::map<int, cudaGraphExec_t> cycle_graphs;  // per KC
+
+    ~Hier();
+    void* dalloc(size_t bytes_);
+    void ensure_workspace(int kc);
+    void ensure_fallback(int kc);
+};
+
+// Solve a device block B (n0 x kc row-major, already in h.B) into h.X.
+// bnorm/state of columns are derived from h.B.  res_out: kc residuals (host).
+void solve_block(Hier& h, int kc, int ncols, const CfSolveParams& p, double* res_out,
+                 CfSolveStats& st);
+// Transposes between rows layout (cnt x n) and block layout (n x kc).
+void rows_to_block(Hier& h, const double* S_dev, int cnt, int kc, double* B_dev);
+void block_to_rows(Hier& h, const double* B_dev, int cnt, int kc, double* S_dev);
+// Column sums over level-0 n x kc block -> h.sums (device), one quantity.
+void colsum_dev(Hier& h, const double* X_dev, int kc, double* out_dev);
+// out[q*kc + c] = sum_p parts[q*qstride + p*kc + c]
+void finalize_dev(Hier& h, const double* parts, int64_t nparts, int nq, int64_t qstride,
+                  double* out, int kc);
+
+}  // namespace cf

@@ -1,0 +1,1316 @@
+// Batched multigrid solve on the device (reference: pkg/src/cfcent/solver.py).
+//
+// One V-cycle (solver.py:526-560) is a fixed sequence of kernels per level:
+//   aggregation level : multicolour forward GS (nu1 sweeps, first from zero)
+//                       -> fused residual + restriction by aggregate
+//                       -> coarse cycle -> line-search reductions
+//                       -> correction x += alpha P xc -> nu2 backward sweeps
+//   elimination level : exact restriction bc = b_c + W_cf D_f^-1 b_f
+//                       -> coarse cycle -> exact interpolation
+//   coarsest          : x = M b with M the centred grounded inverse
+// The outer block iteration (solver.py:651-751) keeps per-column state on the
+// device: residual norms, stagnation counters and the freeze mask.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "cf_common.h"
+#include "cf_hier.h"
+#include "cf_kernels.cuh"
+#include "cfcent_b200.h"
+
+namespace cf {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& m) { g_last_error = m; }
+
+enum ColState { COL_ZERO = 0, COL_ACTIVE = 1, COL_CONV = 2, COL_FALLBACK = 3 };
+
+// ============================================================================
+// kernels
+// ============================================================================
+
+#define CF_LANE_SETUP(KC)                                     \
+    using Lt = Lay<KC>;                                       \
+    constexpr int V = Lt::VEC;                                \
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5; \
+    const int slot = warp * Lt::RPW + lane / Lt::LPR;         \
+    const int c0 = (lane % Lt::LPR) * V;                      \
+    (void)slot;                                               \
+    (void)c0;
+
+// R = B - L X ; partials of sum(R), sum(R^2)  (solver.py:694-695)
+template <int KC>
+__global__ void __launch_bounds__(kThreads) k_residual(int n, const int64_t* __restrict__ rp,
+                                                       const int32_t* __restrict__ col,
+                                                       const double* __restrict__ val,
+                                                       const double* __restrict__ diag,
+                                                       const double* __restrict__ B,
+                                                       const double* __restrict__ X,
+                                                       double* __restrict__ R,
+                                                       double* __restrict__ parts,
+                                                       int64_t nparts) {
+    CF_LANE_SETUP(KC)
+    extern __shared__ double smem[];
+    DV<V> loc[2];
+    zero(loc[0]);
+    zero(loc[1]);
+    const int64_t part = blockIdx.x;
+    for (int r = slot; r < kRowsPerPart; r += Lt::RPB) {
+        int64_t i = part * kRowsPerPart + r;
+        if (i >= n) break;
+        DV<V> acc;
+        zero(acc);
+        gather_row<KC, false>(col, val, rp[i], rp[i + 1], nullptr, X, c0, acc);
+        DV<V> b = ldv<V>(B + i * KC + c0), x = ldv<V>(X + i * KC + c0);
+        double d = diag[i];
+        DV<V> out;
+#pragma unroll
+        for (int t = 0; t < V; ++t) {
+            double v = b.v[t] - fma(d, x.v[t], acc.v[t]);
+            out.v[t] = v;
+            loc[0].v[t] += v;
+            loc[1].v[t] = fma(v, v, loc[1].v[t]);
+        }
+        if (R) stv<V>(R + i * KC + c0, out);
+    }
+    cta_reduce_store<KC, 2>(loc, smem, parts, nparts, part);
+}
+
+// Y = L X (full Laplacian product) -- fallback Krylov solvers (solver.py:571-648)
+template <int KC>
+__global__ void __launch_bounds__(kThreads) k_spmm(int n, const int64_t* __restrict__ rp,
+                                                   const int32_t* __restrict__ col,
+                                                   const double* __restrict__ val,
+                                                   const double* __restrict__ diag,
+                                                   const double* __restrict__ X,
+                                                   double* __restrict__ Y) {
+    CF_LANE_SETUP(KC)
+    int64_t i = (int64_t)blockIdx.x * Lt::RPB + slot;
+    if (i >= n) return;
+    DV<V> acc;
+    zero(acc);
+    gather_row<KC, false>(col, val, rp[i], rp[i + 1], nullptr, X, c0, acc);
+    DV<V> x = ldv<V>(X + i * KC + c0);
+    double d = diag[i];
+#pragma unroll
+    for (int t = 0; t < V; ++t) acc.v[t] = fma(d, x.v[t], acc.v[t]);
+    stv<V>(Y + i * KC + c0, acc);
+}
+
+// partials of sum(b), sum|b|, sum(b^2) (balance check + norms, solver.py:672-679)
+template <int KC>
+__global__ void __launch_bounds__(kThreads) k_colstats(int n, const double* __restrict__ B,
+                                                       double* __restrict__ parts,
+                                                       int64_t nparts) {
+    CF_LANE_SETUP(KC)
+    extern __shared__ double smem[];
+    DV<V> loc[3];
+    zero(loc[0]);
+    zero(loc[1]);
+    zero(loc[2]);
+    const int64_t part = blockIdx.x;
+    for (int r = slot; r < kRowsPerPart; r += Lt::RPB) {
+        int64_t i = part * kRowsPerPart + r;
+        if (i >= n) break;
+        DV<V> b = ldv<V>(B + i * KC + c0);
+#pragma unroll
+        for (int t = 0; t < V; ++t) {
+            loc[0].v[t] += b.v[t];
+            loc[1].v[t] += fabs(b.v[t]);
+            loc[2].v[t] = fma(b.v[t], b.v[t], loc[2].v[t]);
+        }
+    }
+    cta_reduce_store<KC, 3>(loc, smem, parts, nparts, part);
+}
+
+// partials of sum(U1*V1), sum(U2*V2) (fallback dot products)
+template <int KC>
+__global__ void __launch_bounds__(kThreads) k_dot2(int n, const double* __restrict__ U1,
+                                                   const double* __restrict__ V1,
+                                                   const double* __restrict__ U2,
+                                                   const double* __restrict__ V2,
+                                                   double* __restrict__ parts, int64_t nparts) {
+    CF_LANE_SETUP(KC)
+    extern __shared__ double smem[];
+    DV<V> loc[2];
+    zero(loc[0]);
+    zero(loc[1]);
+    const int64_t part = blockIdx.x;
+    for (int r = slot; r < kRowsPerPart; r += Lt::RPB) {
+        int64_t i = part * kRowsPerPart + r;
+        if (i >= n) break;
+        DV<V> a = ldv<V>(U1 + i * KC + c0), b = ldv<V>(V1 + i * KC + c0);
+        DV<V> c = ldv<V>(U2 + i * KC + c0), d = ldv<V>(V2 + i * KC + c0);
+#pragma unroll
+        for (int t = 0; t < V; ++t) {
+            loc[0].v[t] = fma(a.v[t], b.v[t], loc[0].v[t]);
+            loc[1].v[t] = fma(c.v[t], d.v[t], loc[1].v[t]);
+        }
+    }
+    cta_reduce_store<KC, 2>(loc, smem, parts, nparts, part);
+}
+
+// partials of column sums of X (+ Y if given, formed as fl(X+Y))
+template <int KC>
+__global__ void __launch_bounds__(kThreads) k_colsum(int n, const double* __restrict__ X,
+                                                     const double* __restrict__ Y,
+                                                     double* __restrict__ parts,
+                                                     int64_t nparts) {
+    CF_LANE_SETUP(KC)
+    extern __shared__ double smem[];
+    DV<V> loc[1];
+    zero(loc[0]);
+    const int64_t part = blockIdx.x;
+    for (int r = slot; r < kRowsPerPart; r += Lt::RPB) {
+        int64_t i = part * kRowsPerPart + r;
+        if (i >= n) break;
+        DV<V> x = ldv<V>(X + i * KC + c0);
+        if (Y) {
+            DV<V> y = ldv<V>(Y + i * KC + c0);
+#pragma unroll
+            for (int t = 0; t < V; ++t) x.v[t] = x.v[t] + y.v[t];
+        }
+#pragma unroll
+        for (int t = 0; t < V; ++t) loc[0].v[t] += x.v[t];
+    }
+    cta_reduce_store<KC, 1>(loc, smem, parts, nparts, part);
+}
+
+// out[q*KC + c] = sum_p parts[q*qstride + p*KC + c]  (fixed order)
+template <int KC>
+__global__ void __launch_bounds__(kThreads) k_finalize(const double* __restrict__ parts,
+                                                       int64_t nparts, int64_t qstride,
+                                                       double* __restrict__ out) {
+    constexpr int NSEG = kThreads / KC;
+    __shared__ double sm[kThreads];
+    const int q = blockIdx.x;
+    const int c = threadIdx.x % KC, seg = threadIdx.x / KC;
+    const double* p0 = parts + (size_t)q * qstride;
+    int64_t per = (nparts + NSEG - 1) / NSEG;
+    int64_t beg = seg * per, end = min(nparts, beg + per);
+    double s = 0.0;
+    for (int64_t p = beg; p < end; ++p) s += p0[p * KC + c];
+    sm[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x < KC) {
+        double t = 0.0;
+        for (int g = 0; g < NSEG; ++g) t += sm[g * KC + c];
+        out[q * KC + c] = t;
+    }
+}
+
+// Per-column outer-iteration bookkeeping (solver.py:693-715).
+// sums[0..KC) = sum(R), sums[KC..2KC) = sum(R^2).
+template <int KC>
+__global__ void k_status(int n, const double* __restrict__ sums, const double* __restrict__ bn,
+                         double* __restrict__ res, double* __restrict__ prev,
+                         int* __restrict__ stall, int* __restrict__ state,
+                         double* __restrict__ mean, int* __restrict__ count, double stop,
+                         double sfac, int scyc, int final_check) {
+    int c = threadIdx.x;
+    int a = 0;
+    if (c < KC) {
+    if (state[c] == COL_ACTIVE) {
+        double r = sqrt(sums[KC + c]) / bn[c];
+        res[c] = r;
+        bool conv = r <= stop;
+        if (!final_check) {
+            double f = r / prev[c];
+            stall[c] = f > sfac ? stall[c] + 1 : 0;
+            prev[c] = r;
+            bool stuck = stall[c] >= scyc;
+            if (conv)
+                state[c] = COL_CONV;
+            else if (stuck)
+                state[c] = COL_FALLBACK;
+        } else {
+            state[c] = conv ? COL_CONV : COL_FALLBACK;
+        }
+    }
+    mean[c] = sums[c] / (double)n;
+    a = (state[c] == COL_ACTIVE) ? 1 : 0;
+    }
+    // deterministic count (integer)
+    a = __syncthreads_count(a);
+    if (c == 0) *count = a;
+}
+
+// R -= mean (per column)  (solver.py:567-568 _center)
+template <int KC>
+__global__ void __launch_bounds__(kThreads) k_center(int n, double* __restrict__ R,
+                                                     const double* __restrict__ mean) {
+    CF_LANE_SETUP(KC)
+    int64_t i = (int64_t)blockIdx.x * Lt::RPB + slot;
+    if (i >= n) return;
+    DV<V> r = ldv_c<V>(R + i * KC + c0);
+#pragma unroll
+    for (int t = 0; t < V; ++t) r.v[t] = r.v[t] - mean[c0 + t];
+    stv<V>(R + i * KC + c0, r);
+}
+
+// X = fl(X + C) - mean for columns in state ACTIVE (solver.py:708-709)
+template <int KC>
+__global__ void __launch_bounds__(kThreads) k_update(int n, double* __restrict__ X,
+                                                     const double* __restrict__ C,
+                                                     const double* __restrict__ csum,
+                                                     const int* __restrict__ state) {
+    CF_LANE_SETUP(KC)
+    int64_t i = (int64_t)blockIdx.x * Lt::RPB + slot;
+    if (i >= n) return;
+    DV<V> x = ldv_c<V>(X + i * KC + c0), c = ldv<V>(C + i * KC + c0);
+#pragma unroll
+    for (int t = 0; t < V; ++t)
+        if (state[c0 + t] == COL_ACTIVE) x.v[t] = (x.v[t] + c.v[t]) - csum[c0 + t] / (double)n;
+    stv<V>(X + i * KC + c0, x);
+}
+
+// Y = a*Y + b*U + d*W with per-column coefficients coef[0|1|2][KC]
+template <int KC>
+__global__ void __launch_bounds__(kThreads) k_lincomb(int n, double* __restrict__ Y,
+                                                      const double* __restrict__ U,
+                                                      const double* __restrict__ W,
+                                                      const double* __restrict__ coef) {
+    CF_LANE_SETUP(KC)
+    int64_t i = (int64_t)blockIdx.x * Lt::RPB + slot;
+    if (i >= n) return;
+    DV<V> y = ldv_c<V>(Y + i * KC + c0);
+    DV<V> u, w;
+    if (U) u = ldv_c<V>(U + i * KC + c0); else zero(u);
+    if (W) w = ldv_c<V>(W + i * KC + c0); else zero(w);
+#pragma unroll
+    for (int t = 0; t < V; ++t) {
+        int c = c0 + t;
+        y.v[t] = coef[c] * y.v[t] + coef[KC + c] * u.v[t] + coef[2 * KC + c] * w.v[t];
+    }
+    stv<V>(Y + i * KC + c0, y);
+}
+
+// Multicolour Gauss-Seidel sweep over one colour class:
+// x_i = (b_i - sum_{j != i} L_ij x_j) / L_ii.  Rows of one colour are pairwise
+// non-adjacent, so the class updates in parallel with exactly the values a
+// sequential sweep in colour order would use.  from_zero: x_i = b_i / L_ii.
+template <int KC>
+__global__ void __launch_bounds__(kThreads) k_gs(const int32_t* __restrict__ rows, int cnt,
+                                                 const int64_t* __restrict__ rp,
+                                                 const int32_t* __restrict__ col,
+                                                 const double* __restrict__ val,
+                                                 const double* __restrict__ diag,
+                                                 const double* __restrict__ B,
+                                                 double* __restrict__ X, int from_zero) {
+    CF_LANE_SETUP(KC)
+    int64_t g = (int64_t)blockIdx.x * Lt::RPB + slot;
+    if (g >= cnt) return;
+    int64_t i = rows[g];
+    DV<V> acc;
+    zero(acc);
+    if (!from_zero) gather_row<KC, false>(col, val, rp[i], rp[i + 1], nullptr, X, c0, acc);
+    DV<V> b = ldv<V>(B + i * KC + c0);
+    double d = diag[i];
+#pragma unroll
+    for (int t = 0; t < V; ++t) acc.v[t] = (b.v[t] - acc.v[t]) / d;
+    stv<V>(X + i * KC + c0, acc);
+}
+
+// bc[a] = sum_{i in a} (b_i - L_i x)  (residual fused with P^T, solver.py:548-549)
+template <int KC>
+__global__ void __launch_bounds__(kThreads) k_agg_restrict(
+    int nc, const int32_t* __restrict__ aptr, const int32_t* __restrict__ amem,
+    const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+    const double* __restrict__ val, const double* __restrict__ diag,
+    const double* __restrict__ B, const double* __restrict__ X, double* __restrict__ Bc) {
+    CF_LANE_SETUP(KC)
+    int64_t a = (int64_t)blockIdx.x * Lt::RPB + slot;
+    if (a >= nc) return;
+    DV<V> out;
+    zero(out);
+    for (int q = aptr[a]; q < aptr[a + 1]; ++q) {
+        int64_t i = amem[q];
+        DV<V> acc;
+        zero(acc);
+        gather_row<KC, false>(col, val, rp[i], rp[i + 1], nullptr, X, c0, acc);
+        DV<V> b = ldv<V>(B + i * KC + c0), x = ldv<V>(X + i * KC + c0);
+        double d = diag[i];
+#pragma unroll
+        for (int t = 0; t < V; ++t) out.v[t] += b.v[t] - fma(d, x.v[t], acc.v[t]);
+    }
+    stv<V>(Bc + a * KC + c0, out);
+}
+
+// Line-search partials (solver.py:550-556): den = d . L d with d = P xc over
+// fine rows (CTAs [0, pf)), num = r . d = bc . xc over coarse rows (CTAs [pf, pf+pc)).
+template <int KC>
+__global__ void __launch_bounds__(kThreads) k_agg_ls(
+    int n, int nc, const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+    const double* __restrict__ val, const double* __restrict__ diag,
+    const int32_t* __restrict__ agg, const double* __restrict__ Xc,
+    const double* __restrict__ Bc, double* __restrict__ pden, int64_t pf,
+    double* __restrict__ pnum, int64_t pc) {
+    CF_LANE_SETUP(KC)
+    extern __shared__ double smem[];
+    DV<V> loc[1];
+    zero(loc[0]);
+    if (blockIdx.x < pf) {
+        const int64_t part = blockIdx.x;
+        for (int r = slot; r < kRowsPerPart; r += Lt::RPB) {
+            int64_t i = part * kRowsPerPart + r;
+            if (i >= n) break;
+            DV<V> acc;
+            zero(acc);
+            gather_row<KC, true>(col, val, rp[i], rp[i + 1], agg, Xc, c0, acc);
+            DV<V> d = ldv<V>(Xc + (size_t)agg[i] * KC + c0);
+            double dg = diag[i];
+#pragma unroll
+            for (int t = 0; t < V; ++t) {
+                double ld = fma(dg, d.v[t], acc.v[t]);
+                loc[0].v[t] = fma(d.v[t], ld, loc[0].v[t]);
+            }
+        }
+        cta_reduce_store<KC, 1>(loc, smem, pden, pf, part);
+    } else {
+        const int64_t part = blockIdx.x - pf;
+        for (int r = slot; r < kRowsPerPart; r += Lt::RPB) {
+            int64_t a = part * kRowsPerPart + r;
+            if (a >= nc) break;
+            DV<V> b = ldv<V>(Bc + a * KC + c0), x = ldv<V>(Xc + a * KC + c0);
+#pragma unroll
+            for (int t = 0; t < V; ++t) loc[0].v[t] = fma(b.v[t], x.v[t], loc[0].v[t]);
+        }
+        cta_reduce_store<KC, 1>(loc, smem, pnum, pc, part);
+    }
+}
+
+// x += alpha * P xc, alpha = num/den (1 if den <= 0)  (solver.py:556-557)
+template <int KC>
+__global__ void __launch_bounds__(kThreads) k_agg_correct(int n, const int32_t* __restrict__ agg,
+                                                          double* __restrict__ X,
+                                                          const double* __restrict__ Xc,
+                                                          const double* __restrict__ ls) {
+    CF_LANE_SETUP(KC)
+    int64_t i = (int64_t)blockIdx.x * Lt::RPB + slot;
+    if (i >= n) return;
+    DV<V> x = ldv_c<V>(X + i * KC + c0);
+    DV<V> d = ldv<V>(Xc + (size_t)agg[i] * KC + c0);
+#pragma unroll
+    for (int t = 0; t < V; ++t) {
+        double den = ls[c0 + t], num = ls[KC + c0 + t];
+        double alpha = den > 0.0 ? num / den : 1.0;
+        x.v[t] = fma(d.v[t], alpha, x.v[t]);
+    }
+    stv<V>(X + i * KC + c0, x);
+}
+
+// bc_i = b[c_i] + sum_f W_cf(i,f) * (b_f / d_f)  (solver.py:534-536)
+template <int KC>
+__global__ void __launch_bounds__(kThreads) k_elim_restrict(
+    int nc, const int32_t* __restrict__ cn, const int64_t* __restrict__ wp,
+    const int32_t* __restrict__ wc, const double* __restrict__ wv,
+    const int32_t* __restrict__ fn, const double* __restrict__ fd,
+    const double* __restrict__ B, double* __restrict__ Bc) {
+    CF_LANE_SETUP(KC)
+    int64_t i = (int64_t)blockIdx.x * Lt::RPB + slot;
+    if (i >= nc) return;
+    DV<V> acc;
+    zero(acc);
+    for (int64_t p = wp[i]; p < wp[i + 1]; ++p) {
+        int q = wc[p];
+        double w = wv[p], d = fd[q];
+        DV<V> b = ldv<V>(B + (size_t)fn[q] * KC + c0);
+#pragma unroll
+        for (int t = 0; t < V; ++t) acc.v[t] = fma(w, b.v[t] / d, acc.v[t]);
+    }
+    DV<V> b = ldv<V>(B + (size_t)cn[i] * KC + c0);
+#pragma unroll
+    for (int t = 0; t < V; ++t) acc.v[t] = b.v[t] + acc.v[t];
+    stv<V>(Bc + i * KC + c0, acc);
+}
+
+// x[c_i] = xc_i ; x[f] = (b_f + sum W_fc xc) / d_f   (solver.py:538-541)
+template <int KC>
+__global__ void __launch_bounds__(kThreads) k_elim_interp(
+    int nf, int nc, const int32_t* __restrict__ cn, const int32_t* __restrict__ fn,
+    const int64_t* __restrict__ wp, const int32_t* __restrict__ wc,
+    const double* __restrict__ wv, const double* __restrict__ fd,
+    const double* __restrict__ B, const double* __restrict__ Xc, double* __restrict__ X) {
+    CF_LANE_SETUP(KC)
+    int64_t g = (int64_t)blockIdx.x * Lt::RPB + slot;
+    if (g < nc) {
+        DV<V> x = ldv<V>(Xc + g * KC + c0);
+        stv<V>(X + (size_t)cn[g] * KC + c0, x);
+        return;
+    }
+    g -= nc;
+    if (g >= nf) return;
+    DV<V> acc;
+    zero(acc);
+    gather_row<KC, false>(wc, wv, wp[g], wp[g + 1], nullptr, Xc, c0, acc);
+    int64_t i = fn[g];
+    DV<V> b = ldv<V>(B + i * KC + c0);
+    double d = fd[g];
+#pragma unroll
+    for (int t = 0; t < V; ++t) acc.v[t] = (b.v[t] + acc.v[t]) / d;
+    stv<V>(X + i * KC + c0, acc);
+}
+
+// coarsest: x = M b, M dense n x n (solver.py:406-419 restated as one operator)
+template <int KC>
+__global__ void __launch_bounds__(kThreads) k_dense(int n, const double* __restrict__ M,
+                                                    const double* __restrict__ B,
+                                                    double* __restrict__ X) {
+    CF_LANE_SETUP(KC)
+    int64_t i = (int64_t)blockIdx.x * Lt::RPB + slot;
+    if (i >= n) return;
+    DV<V> acc;
+    zero(acc);
+    const double* m = M + (size_t)i * n;
+    for (int l = 0; l < n; ++l) {
+        double a = __ldg(m + l);
+        DV<V> b = ldv<V>(B + (size_t)l * KC + c0);
+#pragma unroll
+        for (int t = 0; t < V; ++t) acc.v[t] = fma(a, b.v[t], acc.v[t]);
+    }
+    stv<V>(X + i * KC + c0, acc);
+}
+
+// rows layout (cnt x n) -> block (n x KC), zero padding for columns >= cnt
+template <int KC>
+__global__ void k_rows_to_block(const double* __restrict__ S, int cnt, int n,
+                                double* __restrict__ B) {
+    __shared__ double tile[32][33];
+    int i0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+    int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+    for (int r = ty; r < 32; r += 8) {
+        int c = c0 + r, i = i0 + tx;
+        tile[r][tx] = (c < cnt && i < n) ? S[(size_t)c * n + i] : 0.0;
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+        int i = i0 + r, c = c0 + tx;
+        if (i < n && c < KC) B[(size_t)i * KC + c] = tile[tx][r];
+    }
+}
+
+template <int KC>
+__global__ void k_block_to_rows(const double* __restrict__ B, int cnt, int n,
+                                double* __restrict__ S) {
+    __shared__ double tile[32][33];
+    int i0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+    int tx = threadIdx.x, ty = threadIdx.y;
+    for (int r = ty; r < 32; r += 8) {
+        int i = i0 + r, c = c0 + tx;
+        tile[r][tx] = (i < n && c < KC) ? B[(size_t)i * KC + c] : 0.0;
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+        int c = c0 + r, i = i0 + tx;
+        if (c < cnt && i < n) S[(size_t)c * n + i] = tile[tx][r];
+    }
+}
+
+// ============================================================================
+// host-side launch helpers
+// ============================================================================
+
+static inline int64_t nparts_of(int64_t n) { return (n + kRowsPerPart - 1) / kRowsPerPart; }
+template <int KC>
+static inline unsigned grid_rows(int64_t rows) {
+    return (unsigned)std::max<int64_t>(1, (rows + Lay<KC>::RPB - 1) / Lay<KC>::RPB);
+}
+template <int KC, int NQ>
+static inline size_t red_smem() {
+    return sizeof(double) * NQ * Lay<KC>::RPB * KC;
+}
+
+template <int KC>
+static void finalize(Hier& h, const double* parts, int64_t nparts, int nq, int64_t qstride,
+                     double* out) {
+    k_finalize<KC><<<nq, kThreads, 0, h.s>>>(parts, nparts, qstride, out);
+}
+
+template <int KC>
+struct Ops {
+    static void residual(Hier& h, const double* B, const double* X, double* R, double* sums2) {
+        DLevel& l = h.L[0];
+        int64_t np = nparts_of(l.n);
+        k_residual<KC><<<(unsigned)np, kThreads, red_smem<KC, 2>(), h.s>>>(
+            l.n, l.rp, l.col, l.val, l.diag, B, X, R, h.parts, np);
+        finalize<KC>(h, h.parts, np, 2, np * KC, sums2);
+    }
+    static void colsum(Hier& h, const double* X, const double* Y, double* out) {
+        int n = h.n0;
+        int64_t np = nparts_of(n);
+        k_colsum<KC><<<(unsigned)np, kThreads, red_smem<KC, 1>(), h.s>>>(n, X, Y, h.parts, np);
+        finalize<KC>(h, h.parts, np, 1, np * KC, out);
+    }
+    static void dot2(Hier& h, const double* a, const double* b, const double* c, const double* d,
+                     double* out) {
+        int n = h.n0;
+        int64_t np = nparts_of(n);
+        k_dot2<KC><<<(unsigned)np, kThreads, red_smem<KC, 2>(), h.s>>>(n, a, b, c, d, h.parts,
+                                                                      np);
+        finalize<KC>(h, h.parts, np, 2, np * KC, out);
+    }
+    static void spmm(Hier& h, const double* X, double* Y) {
+        DLevel& l = h.L[0];
+        k_spmm<KC><<<grid_rows<KC>(l.n), kThreads, 0, h.s>>>(l.n, l.rp, l.col, l.val, l.diag, X,
+                                                             Y);
+    }
+    static void center(Hier& h, double* X, const double* mean) {
+        k_center<KC><<<grid_rows<KC>(h.n0), kThreads, 0, h.s>>>(h.n0, X, mean);
+    }
+    static void lincomb(Hier& h, double* Y, const double* U, const double* W, const double* coef) {
+        k_lincomb<KC><<<grid_rows<KC>(h.n0), kThreads, 0, h.s>>>(h.n0, Y, U, W, coef);
+    }
+
+    static double* bufb(Hier& h, int j) { return j == 0 ? h.R : h.L[j].b; }
+    static double* bufx(Hier& h, int j) { return j == 0 ? h.C : h.L[j].x; }
+
+    // One V-cycle from zero on level j: x_j = cycle(b_j)  (solver.py:526-560)
+    static void cycle(Hier& h, int j, int nu1, int nu2) {
+        DLevel& l = h.L[j];
+        double* b = bufb(h, j);
+        double* x = bufx(h, j);
+        if (l.kind == CF_LEVEL_COARSEST) {
+            if (l.n == 1 || !l.M) {
+                CF_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * (size_t)l.n * KC, h.s));
+            } else {
+                k_dense<KC><<<grid_rows<KC>(l.n), kThreads, 0, h.s>>>(l.n, l.M, b, x);
+            }
+            return;
+        }
+        DLevel& c = h.L[j + 1];
+        double* bc = bufb(h, j + 1);
+        double* xc = bufx(h, j + 1);
+        if (l.kind == CF_LEVEL_ELIMINATION) {
+            k_elim_restrict<KC><<<grid_rows<KC>(l.nc), kThreads, 0, h.s>>>(
+                l.nc, l.cn, l.wcp, l.wcc, l.wcv, l.fn, l.fd, b, bc);
+            cycle(h, j + 1, nu1, nu2);
+            k_elim_interp<KC><<<grid_rows<KC>((int64_t)l.nc + l.nf), kThreads, 0, h.s>>>(
+                l.nf, l.nc, l.cn, l.fn, l.wfp, l.wfc, l.wfv, l.fd, b, xc, x);
+            return;
+        }
+        // aggregation level
+        CF_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * (size_t)l.n * KC, h.s));
+        for (int s = 0; s < nu1; ++s)
+            for (int col = 0; col < l.ncolors; ++col) sweep(h, l, col, b, x, s == 0 && col == 0);
+        k_agg_restrict<KC><<<grid_rows<KC>(l.nc), kThreads, 0, h.s>>>(
+            l.nc, l.aptr, l.amem, l.rp, l.col, l.val, l.diag, b, x, bc);
+        cycle(h, j + 1, nu1, nu2);
+        int64_t pf = nparts_of(l.n), pc = nparts_of(l.nc);
+        k_agg_ls<KC><<<(unsigned)(pf + pc), kThreads, red_smem<KC, 1>(), h.s>>>(
+            l.n, l.nc, l.rp, l.col, l.val, l.diag, l.agg, xc, bc, h.parts, pf,
+            h.parts + pf * KC, pc);
+        finalize<KC>(h, h.parts, pf, 1, 0, l.ls);
+        finalize<KC>(h, h.parts + pf * KC, pc, 1, 0, l.ls + KC);
+        k_agg_correct<KC><<<grid_rows<KC>(l.n), kThreads, 0, h.s>>>(l.n, l.agg, x, xc, l.ls);
+        for (int s = 0; s < nu2; ++s)
+            for (int col = l.ncolors - 1; col >= 0; --col) sweep(h, l, col, b, x, false);
+        (void)c;
+    }
+    static void sweep(Hier& h, DLevel& l, int colr, const double* b, double* x, bool from_zero) {
+        int beg = l.cptr[colr], cnt = l.cptr[colr + 1] - beg;
+        if (cnt <= 0) return;
+        k_gs<KC><<<grid_rows<KC>(cnt), kThreads, 0, h.s>>>(l.crows + beg, cnt, l.rp, l.col, l.val,
+                                                         l.diag, b, x, from_zero ? 1 : 0);
+    }
+
+    static void run_cycle(Hier& h, int nu1, int nu2) {
+        auto it = h.cycle_graphs.find(KC * 1000000 + nu1 * 1000 + nu2);
+        if (it == h.cycle_graphs.end()) {
+            cudaGraph_t g;
+            CF_CUDA(cudaStreamBeginCapture(h.s, cudaStreamCaptureModeThreadLocal));
+            try {
+                cycle(h, 0, nu1, nu2);
+            } catch (...) {
+                cudaStreamEndCapture(h.s, &g);
+                throw;
+            }
+            CF_CUDA(cudaStreamEndCapture(h.s, &g));
+            cudaGraphExec_t ge;
+            CF_CUDA(cudaGraphInstantiate(&ge, g, 0));
+            CF_CUDA(cudaGraphDestroy(g));
+            it = h.cycle_graphs.emplace(KC * 1000000 + nu1 * 1000 + nu2, ge).first;
+        }
+        CF_CUDA(cudaGraphLaunch(it->second, h.s));
+    }
+
+    // --------------------------------------------------------------------
+    // Fallback: V-cycle preconditioned flexible CG (solver.py:571-610) and
+    // Jacobi-preconditioned CG (solver.py:613-648) on the masked columns.
+    // Rare path: per-column scalars are formed on the host.
+    static void host_sums(Hier& h, int nq, double* out) {
+        CF_CUDA(cudaMemcpyAsync(out, h.sums, sizeof(double) * nq * KC, cudaMemcpyDeviceToHost,
+                                h.s));
+        CF_CUDA(cudaStreamSynchronize(h.s));
+    }
+    static void set_coef(Hier& h, const std::vector<double>& coef) {
+        CF_CUDA(cudaMemcpyAsync(h.coef, coef.data(), sizeof(double) * 3 * KC,
+                                cudaMemcpyHostToDevice, h.s));
+    }
+    static void center_cols(Hier& h, double* Xd, const std::vector<char>& mask) {
+        // X[:, mask] -= mean(X[:, mask])
+        colsum(h, Xd, nullptr, h.sums);
+        std::vector<double> s(KC);
+        host_sums(h, 1, s.data());
+        std::vector<double> coef(3 * KC, 0.0);
+        for (int c = 0; c < KC; ++c) {
+            coef[c] = 1.0;
+            coef[KC + c] = mask[c] ? -s[c] / (double)h.n0 : 0.0;
+        }
+        // Y = Y + (-mean) * ones : use W = nullptr, U = ones? implement via lincomb on a ones buffer
+        set_coef(h, coef);
+        k_add_const(h, Xd);
+    }
+    static void k_add_const(Hier& h, double* Xd);
+    static void column_res(Hier& h, const double* Xd, const std::vector<double>& bn,
+                           const std::vector<char>& mask, std::vector<double>& res) {
+        residual(h, h.B, Xd, nullptr, h.sums);
+        std::vector<double> s(2 * KC);
+        host_sums(h, 2, s.data());
+        for (int c = 0; c < KC; ++c)
+            if (mask[c]) res[c] = std::sqrt(s[KC + c]) / bn[c];
+    }
+
+    static void fcg(Hier& h, const std::vector<double>& bn, double tau, int nu1, int nu2,
+                    int iters, const std::vector<char>& mask0, std::vector<double>& res) {
+        h.ensure_fallback(KC);
+        std::vector<char> active = mask0, have(KC, 0);
+        column_res(h, h.X, bn, active, res);
+        CF_CUDA(cudaMemsetAsync(h.P, 0, sizeof(double) * (size_t)h.n0 * KC, h.s));
+        CF_CUDA(cudaMemsetAsync(h.AP, 0, sizeof(double) * (size_t)h.n0 * KC, h.s));
+        std::vector<double> s(2 * KC), coef(3 * KC);
+        for (int it = 0; it < iters; ++it) {
+            bool any = false;
+            for (int c = 0; c < KC; ++c) {
+                active[c] = active[c] && res[c] > tau;
+                any = any || active[c];
+            }
+            if (!any) break;
+            // r = center(b - L x)
+            residual(h, h.B, h.X, h.R, h.sums);
+            host_sums(h, 2, s.data());
+            for (int c = 0; c < KC; ++c) s[c] = s[c] / (double)h.n0;
+            CF_CUDA(cudaMemcpyAsync(h.sums + 4 * KC, s.data(), sizeof(double) * KC,
+                                    cudaMemcpyHostToDevice, h.s));
+            center(h, h.R, h.sums + 4 * KC);
+            // z = center(cycle(r))
+            run_cycle(h, nu1, nu2);
+            colsum(h, h.C, nullptr, h.sums);
+            host_sums(h, 1, s.data());
+            for (int c = 0; c < KC; ++c) s[c] = s[c] / (double)h.n0;
+            CF_CUDA(cudaMemcpyAsync(h.sums + 4 * KC, s.data(), sizeof(double) * KC,
+                                    cudaMemcpyHostToDevice, h.s));
+            center(h, h.C, h.sums + 4 * KC);
+            // beta for columns with a previous direction
+            dot2(h, h.C, h.AP, h.P, h.AP, h.sums);
+            host_sums(h, 2, s.data());
+            for (int c = 0; c < KC; ++c) {
+                double beta = 0.0;
+                if (active[c] && have[c]) {
+                    double zl = s[c], dl = s[KC + c];
+                    beta = dl > 0 ? zl / dl : 0.0;
+                }
+                coef[c] = 1.0;
+                coef[KC + c] = -beta;
+                coef[2 * KC + c] = 0.0;
+            }
+            set_coef(h, coef);
+            lincomb(h, h.C, h.P, nullptr, h.coef);  // z -= beta p
+            // p = z (active), Lp = L z
+            for (int c = 0; c < KC; ++c) {
+                coef[c] = active[c] ? 0.0 : 1.0;
+                coef[KC + c] = active[c] ? 1.0 : 0.0;
+                coef[2 * KC + c] = 0.0;
+            }
+            set_coef(h, coef);
+            lincomb(h, h.P, h.C, nullptr, h.coef);
+            spmm(h, h.P, h.Z);
+            lincomb(h, h.AP, h.Z, nullptr, h.coef);
+            for (int c = 0; c < KC; ++c) have[c] = have[c] || active[c];
+            // alpha = (r.z)/(z.Lz)
+            dot2(h, h.C, h.AP, h.R, h.C, h.sums);
+            host_sums(h, 2, s.data());
+            for (int c = 0; c < KC; ++c) {
+                double dl = s[c], rd = s[KC + c];
+                double alpha = (active[c] && dl > 0) ? rd / dl : 0.0;
+                coef[c] = 1.0;
+                coef[KC + c] = active[c] ? alpha : 0.0;
+                coef[2 * KC + c] = 0.0;
+            }
+            set_coef(h, coef);
+            lincomb(h, h.X, h.C, nullptr, h.coef);
+            center_cols(h, h.X, active);
+            column_res(h, h.X, bn, active, res);
+        }
+    }
+
+    static void jpcg(Hier& h, const std::vector<double>& bn, double tau, int iters,
+                     const std::vector<char>& mask, std::vector<double>& res) {
+        h.ensure_fallback(KC);
+        // Z holds D^-1 (as a column-broadcast the kernel would need); use lincomb with
+        // a diagonal-scaling pass instead: k_diag_scale.
+        std::vector<double> s(2 * KC), coef(3 * KC), rz(KC), rz2(KC);
+        // r = center(b - L x)
+        residual(h, h.B, h.X, h.R, h.sums);
+        host_sums(h, 2, s.data());
+        for (int c = 0; c < KC; ++c) s[c] = s[c] / (double)h.n0;
+        CF_CUDA(cudaMemcpyAsync(h.sums + 4 * KC, s.data(), sizeof(double) * KC,
+                                cudaMemcpyHostToDevice, h.s));
+        center(h, h.R, h.sums + 4 * KC);
+        diag_scale(h, h.R, h.Z);  // z = D^-1 r
+        CF_CUDA(cudaMemcpyAsync(h.P, h.Z, sizeof(double) * (size_t)h.n0 * KC,
+                                cudaMemcpyDeviceToDevice, h.s));
+        dot2(h, h.R, h.Z, h.R, h.Z, h.sums);
+        host_sums(h, 2, s.data());
+        for (int c = 0; c < KC; ++c) rz[c] = s[c];
+        std::vector<char> all = mask;
+        column_res(h, h.X, bn, all, res);
+        std::vector<char> frozen(KC, 1);
+        for (int c = 0; c < KC; ++c) frozen[c] = !mask[c] || res[c] <= tau;
+        for (int it = 0; it < iters; ++it) {
+            bool done = true;
+            for (int c = 0; c < KC; ++c) done = done && frozen[c];
+            if (done) break;
+            spmm(h, h.P, h.AP);
+            dot2(h, h.P, h.AP, h.P, h.AP, h.sums);
+            host_sums(h, 2, s.data());
+            std::vector<double> alpha(KC, 0.0);
+            for (int c = 0; c < KC; ++c) {
+                double plp = s[c];
+                alpha[c] = (plp > 0 && !frozen[c]) ? rz[c] / plp : 0.0;
+                coef[c] = 1.0;
+                coef[KC + c] = alpha[c];
+                coef[2 * KC + c] = 0.0;
+            }
+            set_coef(h, coef);
+            lincomb(h, h.X, h.P, nullptr, h.coef);  // x += alpha p
+            for (int c = 0; c < KC; ++c) coef[KC + c] = -alpha[c];
+            set_coef(h, coef);
+            lincomb(h, h.R, h.AP, nullptr, h.coef);  // r -= alpha Lp
+            dot2(h, h.R, h.R, h.R, h.R, h.sums);
+            host_sums(h, 2, s.data());
+            for (int c = 0; c < KC; ++c) {
+                if (mask[c]) res[c] = std::sqrt(s[c]) / bn[c];
+                frozen[c] = frozen[c] || !mask[c] || res[c] <= tau;
+            }
+            diag_scale(h, h.R, h.Z);
+            dot2(h, h.R, h.Z, h.R, h.Z, h.sums);
+            host_sums(h, 2, s.data());
+            for (int c = 0; c < KC; ++c) {
+                rz2[c] = s[c];
+                double beta = rz[c] > 0 ? rz2[c] / rz[c] : 0.0;
+                if (frozen[c]) beta = 0.0;
+                coef[c] = beta;  // p = z + beta p
+                coef[KC + c] = 1.0;
+                coef[2 * KC + c] = 0.0;
+            }
+            set_coef(h, coef);
+            lincomb(h, h.P, h.Z, nullptr, h.coef);
+            rz = rz2;
+        }
+        center_cols(h, h.X, mask);
+        column_res(h, h.X, bn, mask, res);
+    }
+    static void diag_scale(Hier& h, const double* Rd, double* Zd);
+};
+
+template <int KC>
+__global__ void __launch_bounds__(kThreads) k_diag_scale(int n, const double* __restrict__ diag,
+                                                         const double* __restrict__ R,
+                                                         double* __restrict__ Z) {
+    CF_LANE_SETUP(KC)
+    int64_t i = (int64_t)blockIdx.x * Lt::RPB + slot;
+    if (i >= n) return;
+    DV<V> r = ldv_c<V>(R + i * KC + c0);
+    double dinv = 1.0 / fmax(diag[i], 2.2250738585072014e-308);
+#pragma unroll
+    for (int t = 0; t < V; ++t) r.v[t] = dinv * r.v[t];
+    stv<V>(Z + i * KC + c0, r);
+}
+
+// X[:, c] += coef[KC + c]  (coef[c] ignored)
+template <int KC>
+__global__ void __launch_bounds__(kThreads) k_addc(int n, double* __restrict__ X,
+                                                   const double* __restrict__ coef) {
+    CF_LANE_SETUP(KC)
+    int64_t i = (int64_t)blockIdx.x * Lt::RPB + slot;
+    if (i >= n) return;
+    DV<V> x = ldv_c<V>(X + i * KC + c0);
+#pragma unroll
+    for (int t = 0; t < V; ++t) x.v[t] = x.v[t] + coef[KC + c0 + t];
+    stv<V>(X + i * KC + c0, x);
+}
+
+template <int KC>
+void Ops<KC>::diag_scale(Hier& h, const double* Rd, double* Zd) {
+    k_diag_scale<KC><<<grid_rows<KC>(h.n0), kThreads, 0, h.s>>>(h.n0, h.L[0].diag, Rd, Zd);
+}
+template <int KC>
+void Ops<KC>::k_add_const(Hier& h, double* Xd) {
+    k_addc<KC><<<grid_rows<KC>(h.n0), kThreads, 0, h.s>>>(h.n0, Xd, h.coef);
+}
+
+// ============================================================================
+// block solve driver (solver.py:651-751)
+// ============================================================================
+
+template <int KC>
+static void solve_block_t(Hier& h, int ncols, const CfSolveParams& p, double* res_out,
+                          CfSolveStats& st) {
+    const int n = h.n0;
+    using O = Ops<KC>;
+    // column statistics of B: balance check and norms (solver.py:672-679)
+    {
+        int64_t np = nparts_of(n);
+        k_colstats<KC><<<(unsigned)np, kThreads, red_smem<KC, 3>(), h.s>>>(n, h.B, h.parts, np);
+        finalize<KC>(h, h.parts, np, 3, np * KC, h.sums);
+        CF_CUDA(cudaMemcpyAsync(h.h_small, h.sums, sizeof(double) * 3 * KC,
+                                cudaMemcpyDeviceToHost, h.s));
+        CF_CUDA(cudaStreamSynchronize(h.s));
+    }
+    std::vector<double> bsum(KC), bl1(KC), bn(KC);
+    std::vector<int> bad;
+    for (int c = 0; c < KC; ++c) {
+        bsum[c] = h.h_small[c];
+        bl1[c] = h.h_small[KC + c];
+        bn[c] = std::sqrt(h.h_small[2 * KC + c]);
+        if (c < ncols && std::fabs(bsum[c]) > 1e-10 * std::max(bl1[c], 2.2250738585072014e-308))
+            bad.push_back(c);
+    }
+    if (!bad.empty()) {
+        std::string m = "supply vector columns [";
+        for (size_t q = 0; q < bad.size(); ++q) m += (q ? ", " : "") + std::to_string(bad[q]);
+        throw CfError(CF_DOMAIN, m + "] are not balanced");
+    }
+    // per-column state
+    std::vector<int> state(KC, COL_ZERO);
+    std::vector<double> safe(KC, 1.0), prev(KC, INFINITY), res(KC, 0.0);
+    int nactive = 0;
+    for (int c = 0; c < ncols; ++c)
+        if (bn[c] > 0) {
+            state[c] = COL_ACTIVE;
+            safe[c] = bn[c];
+            ++nactive;
+        }
+    CF_CUDA(cudaMemsetAsync(h.X, 0, sizeof(double) * (size_t)n * KC, h.s));
+    const double tau = p.tau, stop = p.stop_margin * p.tau;
+    std::vector<int> zeros(KC, 0);
+    CF_CUDA(cudaMemcpyAsync(h.bn, safe.data(), sizeof(double) * KC, cudaMemcpyHostToDevice, h.s));
+    CF_CUDA(cudaMemcpyAsync(h.prev, prev.data(), sizeof(double) * KC, cudaMemcpyHostToDevice, h.s));
+    CF_CUDA(cudaMemcpyAsync(h.stall, zeros.data(), sizeof(int) * KC, cudaMemcpyHostToDevice, h.s));
+    CF_CUDA(cudaMemcpyAsync(h.state, state.data(), sizeof(int) * KC, cudaMemcpyHostToDevice, h.s));
+    CF_CUDA(cudaMemsetAsync(h.res, 0, sizeof(double) * KC, h.s));
+    double* mean = h.sums + 2 * KC;
+    double* csum = h.sums + 3 * KC;
+    int64_t fallback_cols = 0;
+    if (nactive > 0) {
+        bool broke = false;
+        for (int it = 0; it < p.max_cycles; ++it) {
+            O::residual(h, h.B, h.X, h.R, h.sums);
+            k_status<KC><<<1, KC < 32 ? 32 : KC, 0, h.s>>>(n, h.sums, h.bn, h.res, h.prev, h.stall,
+                                                            h.state, mean, h.count, stop,
+                                                            p.stagnation_factor,
+                                                            p.stagnation_cycles, 0);
+            CF_CUDA(cudaMemcpyAsync(h.h_count, h.count, sizeof(int), cudaMemcpyDeviceToHost, h.s));
+            CF_CUDA(cudaStreamSynchronize(h.s));
+            int act = *h.h_count;
+            if (act == 0) {
+                broke = true;
+                break;
+            }
+            O::center(h, h.R, mean);
+            O::run_cycle(h, p.nu1, p.nu2);
+            O::colsum(h, h.X, h.C, csum);
+            k_update<KC><<<grid_rows<KC>(n), kThreads, 0, h.s>>>(n, h.X, h.C, csum, h.state);
+            st.vcycles += act;
+            st.outer_iterations += 1;
+        }
+        if (!broke) {
+            O::residual(h, h.B, h.X, h.R, h.sums);
+            k_status<KC><<<1, KC < 32 ? 32 : KC, 0, h.s>>>(n, h.sums, h.bn, h.res, h.prev, h.stall,
+                                                            h.state, mean, h.count, stop,
+                                                            p.stagnation_factor,
+                                                            p.stagnation_cycles, 1);
+        }
+        CF_CUDA(cudaMemcpyAsync(state.data(), h.state, sizeof(int) * KC, cudaMemcpyDeviceToHost,
+                                h.s));
+        CF_CUDA(cudaMemcpyAsync(res.data(), h.res, sizeof(double) * KC, cudaMemcpyDeviceToHost,
+                                h.s));
+        CF_CUDA(cudaStreamSynchronize(h.s));
+        std::vector<char> fb(KC, 0);
+        for (int c = 0; c < KC; ++c)
+            if (state[c] == COL_FALLBACK) {
+                fb[c] = 1;
+                ++fallback_cols;
+            }
+        if (fallback_cols) {
+            std::vector<double> rf(KC, 0.0);
+            O::fcg(h, safe, stop, p.nu1, p.nu2, p.fcg_max_iters, fb, rf);
+            std::vector<char> still(KC, 0);
+            bool any = false;
+            for (int c = 0; c < KC; ++c)
+                if (fb[c] && rf[c] > stop) {
+                    still[c] = 1;
+                    any = true;
+                }
+            if (any) {
+                std::vector<double> rg(rf);
+                O::jpcg(h, safe, stop, p.jpcg_max_iters, still, rg);
+                for (int c = 0; c < KC; ++c)
+                    if (still[c]) rf[c] = rg[c];
+            }
+            double worst = 0.0;
+            int nbad = 0;
+            for (int c = 0; c < KC; ++c)
+                if (fb[c]) {
+                    worst = std::max(worst, rf[c]);
+                    if (rf[c] > tau) ++nbad;
+                }
+            if (nbad) {
+                char buf[160];
+                snprintf(buf, sizeof buf, "%d solve(s) failed to reach tau=%g", nbad, tau);
+                throw CfError(CF_CONVERGENCE, buf, worst);
+            }
+        }
+    }
+    // final centring and independently recomputed residuals (solver.py:748-749)
+    O::colsum(h, h.X, nullptr, csum);
+    {
+        // X -= mean(X) for all columns
+        std::vector<double> s(KC);
+        CF_CUDA(cudaMemcpyAsync(s.data(), csum, sizeof(double) * KC, cudaMemcpyDeviceToHost, h.s));
+        CF_CUDA(cudaStreamSynchronize(h.s));
+        std::vector<double> coef(3 * KC, 0.0);
+        for (int c = 0; c < KC; ++c) coef[KC + c] = -(s[c] / (double)n);
+        CF_CUDA(cudaMemcpyAsync(h.coef, coef.data(), sizeof(double) * 3 * KC,
+                                cudaMemcpyHostToDevice, h.s));
+        O::k_add_const(h, h.X);
+    }
+    O::residual(h, h.B, h.X, nullptr, h.sums);
+    std::vector<double> s2(2 * KC);
+    CF_CUDA(cudaMemcpyAsync(s2.data(), h.sums, sizeof(double) * 2 * KC, cudaMemcpyDeviceToHost,
+                            h.s));
+    CF_CUDA(cudaStreamSynchronize(h.s));
+    for (int c = 0; c < ncols; ++c) {
+        res_out[c] = bn[c] > 0 ? std::sqrt(s2[KC + c]) / bn[c] : 0.0;
+        st.max_residual = std::max(st.max_residual, res_out[c]);
+    }
+    st.solves += ncols;
+    st.fallback_solves += fallback_cols;
+}
+
+int pick_kc(int64_t rem) {
+    static const int sizes[] = {1, 8, 16, 32, 64, 128, 256};
+    if (rem >= 32) {
+        int best = 32;
+        for (int s : sizes)
+            if (s <= rem) best = s;
+        return best;
+    }
+    for (int s : sizes)
+        if (s >= rem) return s;
+    return 256;
+}
+
+static int kc_at_least(int k) {
+    static const int sizes[] = {1, 8, 16, 32, 64, 128, 256};
+    for (int s : sizes)
+        if (s >= k) return s;
+    return 256;
+}
+
+#define CF_DISPATCH(KCV, ...)                        \
+    switch (KCV) {                                    \
+        case 1: { constexpr int K_ = 1; __VA_ARGS__; } break;     \
+        case 8: { constexpr int K_ = 8; __VA_ARGS__; } break;     \
+        case 16: { constexpr int K_ = 16; __VA_ARGS__; } break;   \
+        case 32: { constexpr int K_ = 32; __VA_ARGS__; } break;   \
+        case 64: { constexpr int K_ = 64; __VA_ARGS__; } break;   \
+        case 128: { constexpr int K_ = 128; __VA_ARGS__; } break; \
+        case 256: { constexpr int K_ = 256; __VA_ARGS__; } break; \
+        default: throw CfError(CF_RUNTIME, "unsupported block width"); \
+    }
+
+void solve_block(Hier& h, int kc, int ncols, const CfSolveParams& p, double* res_out,
+                 CfSolveStats& st) {
+    CF_DISPATCH(kc, solve_block_t<K_>(h, ncols, p, res_out, st));
+}
+
+void rows_to_block(Hier& h, const double* S_dev, int cnt, int kc, double* B_dev) {
+    dim3 blk(32, 8), grd((h.n0 + 31) / 32, (kc + 31) / 32);
+    CF_DISPATCH(kc, (k_rows_to_block<K_><<<grd, blk, 0, h.s>>>(S_dev, cnt, h.n0, B_dev)));
+}
+void block_to_rows(Hier& h, const double* B_dev, int cnt, int kc, double* S_dev) {
+    dim3 blk(32, 8), grd((h.n0 + 31) / 32, (kc + 31) / 32);
+    CF_DISPATCH(kc, (k_block_to_rows<K_><<<grd, blk, 0, h.s>>>(B_dev, cnt, h.n0, S_dev)));
+}
+void finalize_dev(Hier& h, const double* parts, int64_t nparts, int nq, int64_t qstride,
+                  double* out, int kc) {
+    CF_DISPATCH(kc, finalize<K_>(h, parts, nparts, nq, qstride, out));
+}
+void colsum_dev(Hier& h, const double* X_dev, int kc, double* out_dev) {
+    CF_DISPATCH(kc, Ops<K_>::colsum(h, X_dev, nullptr, out_dev));
+}
+
+// ============================================================================
+// Hier lifetime
+// ============================================================================
+
+void* Hier::dalloc(size_t nb) {
+    void* p = nullptr;
+    if (nb == 0) nb = 8;
+    CF_CUDA(cudaMalloc(&p, nb));
+    owned.push_back(p);
+    bytes += (int64_t)nb;
+    return p;
+}
+
+Hier::~Hier() {
+    cudaSetDevice(dev);
+    for (auto& kv : cycle_graphs) cudaGraphExecDestroy(kv.second);
+    for (void* p : owned) cudaFree(p);
+    for (auto& l : L) {
+        cudaFree(l.b);
+        cudaFree(l.x);
+    }
+    cudaFree(B);
+    cudaFree(X);
+    cudaFree(R);
+    cudaFree(C);
+    cudaFree(Z);
+    cudaFree(P);
+    cudaFree(AP);
+    cudaFree(parts);
+    cudaFree(S);
+    if (h_count) cudaFreeHost(h_count);
+    if (h_small) cudaFreeHost(h_small);
+    if (s) cudaStreamDestroy(s);
+}
+
+void Hier::ensure_workspace(int kc) {
+    if (kc <= kc_ws) return;
+    for (auto& kv : cycle_graphs) cudaGraphExecDestroy(kv.second);
+    cycle_graphs.clear();
+    CF_CUDA(cudaStreamSynchronize(s));
+    auto re = [&](double*& p, size_t elems) {
+        if (p) {
+            CF_CUDA(cudaFree(p));
+        }
+        p = nullptr;
+        CF_CUDA(cudaMalloc(&p, sizeof(double) * std::max<size_t>(elems, 1)));
+    };
+    for (size_t j = 1; j < L.size(); ++j) {
+        re(L[j].b, (size_t)L[j].n * kc);
+        re(L[j].x, (size_t)L[j].n * kc);
+    }
+    re(B, (size_t)n0 * kc);
+    re(X, (size_t)n0 * kc);
+    re(R, (size_t)n0 * kc);
+    re(C, (size_t)n0 * kc);
+    re(S, (size_t)n0 * kc);
+    size_t np = 0;
+    for (auto& l : L) np = std::max<size_t>(np, (size_t)(nparts_of(l.n) + nparts_of(l.nc) + 2));
+    np = std::max<size_t>(np, 3 * (size_t)(nparts_of(n0) + 1));
+    re(parts, np * kc);
+    parts_cap = np * kc;
+    if (Z) {
+        cudaFree(Z); cudaFree(P); cudaFree(AP);
+        Z = P = AP = nullptr;
+        kc_fb = 0;
+    }
+    kc_ws = kc;
+}
+
+void Hier::ensure_fallback(int kc) {
+    if (kc <= kc_fb) return;
+    auto re = [&](double*& p, size_t elems) {
+        if (p) CF_CUDA(cudaFree(p));
+        p = nullptr;
+        CF_CUDA(cudaMalloc(&p, sizeof(double) * std::max<size_t>(elems, 1)));
+    };
+    re(Z, (size_t)n0 * kc_ws);
+    re(P, (size_t)n0 * kc_ws);
+    re(AP, (size_t)n0 * kc_ws);
+    kc_fb = kc_ws;
+}
+
+}  // namespace cf
+
+using namespace cf;
+
+// ============================================================================
+// C-ABI
+// ============================================================================
+
+extern "C" const char* cf_last_error(void) { return g_last_error.c_str(); }
+extern "C" int cf_version(void) { return 1; }
+extern "C" int cf_device_count(void) {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) return 0;
+    return c;
+}
+
+template <typename T>
+static T* upload(Hier& h, const T* src, size_t cnt) {
+    if (!src || cnt == 0) return nullptr;
+    T* d = (T*)h.dalloc(sizeof(T) * cnt);
+    CF_CUDA(cudaMemcpy(d, src, sizeof(T) * cnt, cudaMemcpyHostToDevice));
+    return d;
+}
+
+extern "C" int cf_hier_create(int32_t nlev, const CfLevelDesc* ds, int32_t device,
+                              void** out) {
+    CF_API_BEGIN
+    if (nlev < 1) throw CfError(CF_DOMAIN, "hierarchy needs at least one level");
+    CF_CUDA(cudaSetDevice(device));
+    auto* h = new Hier();
+    try {
+        h->dev = device;
+        CF_CUDA(cudaStreamCreateWithFlags(&h->s, cudaStreamNonBlocking));
+        h->n0 = ds[0].n;
+        h->L.resize(nlev);
+        for (int j = 0; j < nlev; ++j) {
+            const CfLevelDesc& d = ds[j];
+            DLevel& l = h->L[j];
+            l.kind = d.kind;
+            l.n = d.n;
+            l.nc = d.n_coarse;
+            l.nnz = d.nnz_off;
+            bool need_matrix = (j == 0) || d.kind == CF_LEVEL_AGGREGATION;
+            if (need_matrix && d.rowptr) {
+                l.rp = upload(*h, d.rowptr, (size_t)d.n + 1);
+                l.col = upload(*h, d.col, (size_t)d.nnz_off);
+                l.val = upload(*h, d.val, (size_t)d.nnz_off);
+                if (!l.col) l.col = (int32_t*)h->dalloc(8);
+                if (!l.val) l.val = (double*)h->dalloc(8);
+                l.diag = upload(*h, d.diag, (size_t)d.n);
+            } else if (need_matrix) {
+                throw CfError(CF_DOMAIN, "level matrix missing");
+            }
+            if (d.kind == CF_LEVEL_AGGREGATION) {
+                l.ncolors = d.n_colors;
+                l.cptr.assign(d.color_ptr, d.color_ptr + d.n_colors + 1);
+                l.crows = upload(*h, d.color_rows, (size_t)d.n);
+                l.agg = upload(*h, d.agg, (size_t)d.n);
+                l.aptr = upload(*h, d.agg_ptr, (size_t)d.n_coarse + 1);
+                l.amem = upload(*h, d.agg_members, (size_t)d.n);
+                l.ls = (double*)h->dalloc(sizeof(double) * 2 * kMaxKC);
+            } else if (d.kind == CF_LEVEL_ELIMINATION) {
+                l.nf = d.n_f;
+                l.fn = upload(*h, d.f_nodes, (size_t)d.n_f);
+                l.cn = upload(*h, d.c_nodes, (size_t)d.n_coarse);
+                l.fd = upload(*h, d.f_degree, (size_t)d.n_f);
+                l.wcp = upload(*h, d.wcf_ptr, (size_t)d.n_coarse + 1);
+                l.wcc = upload(*h, d.wcf_col, (size_t)d.wcf_ptr[d.n_coarse]);
+                l.wcv = upload(*h, d.wcf_val, (size_t)d.wcf_ptr[d.n_coarse]);
+                l.wfp = upload(*h, d.wfc_ptr, (size_t)d.n_f + 1);
+                l.wfc = upload(*h, d.wfc_col, (size_t)d.wfc_ptr[d.n_f]);
+                l.wfv = upload(*h, d.wfc_val, (size_t)d.wfc_ptr[d.n_f]);
+                if (!l.wcc) l.wcc = (int32_t*)h->dalloc(8);
+                if (!l.wcv) l.wcv = (double*)h->dalloc(8);
+                if (!l.wfc) l.wfc = (int32_t*)h->dalloc(8);
+                if (!l.wfv) l.wfv = (double*)h->dalloc(8);
+            } else {
+                if (d.coarse_op && d.n > 1) l.M = upload(*h, d.coarse_op, (size_t)d.n * d.n);
+            }
+        }
+        h->sums = (double*)h->dalloc(sizeof(double) * 8 * kMaxKC);
+        h->coef = (double*)h->dalloc(sizeof(double) * 4 * kMaxKC);
+        h->bn = (double*)h->dalloc(sizeof(double) * kMaxKC);
+        h->res = (double*)h->dalloc(sizeof(double) * kMaxKC);
+        h->prev = (double*)h->dalloc(sizeof(double) * kMaxKC);
+        h->stall = (int*)h->dalloc(sizeof(int) * kMaxKC);
+        h->state = (int*)h->dalloc(sizeof(int) * kMaxKC);
+        h->count = (int*)h->dalloc(sizeof(int) * 4);
+        CF_CUDA(cudaMallocHost(&h->h_count, sizeof(int) * 4));
+        CF_CUDA(cudaMallocHost(&h->h_small, sizeof(double) * 16 * kMaxKC));
+    } catch (...) {
+        delete h;
+        throw;
+    }
+    *out = h;
+    CF_API_END
+}
+
+extern "C" int cf_hier_destroy(void* hp) {
+    CF_API_BEGIN
+    delete (Hier*)hp;
+    CF_API_END
+}
+
+extern "C" int64_t cf_hier_device_bytes(void* hp) {
+    Hier* h = (Hier*)hp;
+    int64_t b = h->bytes;
+    for (size_t j = 1; j < h->L.size(); ++j) b += 2 * (int64_t)h->L[j].n * h->kc_ws * 8;
+    b += 5 * (int64_t)h->n0 * h->kc_ws * 8 + (int64_t)h->parts_cap * 8;
+    return b;
+}
+
+extern "C" int cf_solve_rows(void* hp, const double* rows, int64_t count,
+                             const CfSolveParams* p, double* out_rows, double* residuals,
+                             CfSolveStats* st) {
+    CF_API_BEGIN
+    Hier& h = *(Hier*)hp;
+    std::lock_guard<std::mutex> lk(h.mu);
+    CF_CUDA(cudaSetDevice(h.dev));
+    const int64_t n = h.n0;
+    int64_t done = 0;
+    while (done < count) {
+        int kc = pick_kc(count - done);
+        int cnt = (int)std::min<int64_t>(kc, count - done);
+        h.ensure_workspace(kc);
+        CF_CUDA(cudaMemcpyAsync(h.S, rows + done * n, sizeof(double) * cnt * n,
+                                cudaMemcpyHostToDevice, h.s));
+        rows_to_block(h, h.S, cnt, kc, h.B);
+        std::vector<double> res(kc, 0.0);
+        solve_block(h, kc, cnt, *p, res.data(), *st);
+        block_to_rows(h, h.X, cnt, kc, h.S);
+        CF_CUDA(cudaMemcpyAsync(out_rows + done * n, h.S, sizeof(double) * cnt * n,
+                                cudaMemcpyDeviceToHost, h.s));
+        CF_CUDA(cudaStreamSynchronize(h.s));
+        std::memcpy(residuals + done, res.data(), sizeof(double) * cnt);
+        done += cnt;
+    }
+    CF_API_END_STATS(st)
+}
+
+extern "C" int cf_solve_block_dev(void* hp, const double* B_dev, double* X_dev, int32_t k,
+                                  const CfSolveParams* p, double* residuals, CfSolveStats* st) {
+    CF_API_BEGIN
+    Hier& h = *(Hier*)hp;
+    std::lock_guard<std::mutex> lk(h.mu);
+    CF_CUDA(cudaSetDevice(h.dev));
+    if (k < 1 || k > kMaxKC) throw CfError(CF_DOMAIN, "k must be in [1, 256]");
+    int kc = kc_at_least(k);
+    h.ensure_workspace(kc);
+    // B_dev is n x k row-major; widen to kc columns
+    CF_CUDA(cudaMemsetAsync(h.B, 0, sizeof(double) * (size_t)h.n0 * kc, h.s));
+    CF_CUDA(cudaMemcpy2DAsync(h.B, sizeof(double) * kc, B_dev, sizeof(double) * k,
+                              sizeof(double) * k, h.n0, cudaMemcpyDeviceToDevice, h.s));
+    std::vector<double> res(kc, 0.0);
+    solve_block(h, kc, k, *p, res.data(), *st);
+    CF_CUDA(cudaMemcpy2DAsync(X_dev, sizeof(double) * k, h.X, sizeof(double) * kc,
+                              sizeof(double) * k, h.n0, cudaMemcpyDeviceToDevice, h.s));
+    CF_CUDA(cudaStreamSynchronize(h.s));
+    std::memcpy(residuals, res.data(), sizeof(double) * k);
+    CF_API_END_STATS(st)
+}
+
+extern "C" int cf_residual_dev(void* hp, const double* B_dev, const double* X_dev, double* R_dev,
+                               int32_t k, double* colsq) {
+    CF_API_BEGIN
+    Hier& h = *(Hier*)hp;
+    std::lock_guard<std::mutex> lk(h.mu);
+    CF_CUDA(cudaSetDevice(h.dev));
+    int kc = pick_kc(k);
+    if (kc != k) throw CfError(CF_DOMAIN, "k must be a supported block width");
+    h.ensure_workspace(kc);
+    CF_DISPATCH(kc, Ops<K_>::residual(h, B_dev, X_dev, R_dev, h.sums));
+    CF_CUDA(cudaMemcpyAsync(colsq, h.sums + k, sizeof(double) * k, cudaMemcpyDeviceToHost, h.s));
+    CF_CUDA(cudaStreamSynchronize(h.s));
+    CF_API_END
+}

@@ -1,0 +1,197 @@
+"""Generate the golden fixtures by running the REFERENCE package itself.
+
+Run in the build container only (it imports ``/root/reference/pkg/src``,
+which does not exist on the GPU box):
+
+    python tests/golden/make_golden.py
+
+Writes ``tests/golden/*.npz`` (small, committed).  Each fixture records the
+numpy/scipy versions that produced it (RNG-stream provenance).
+"""
+
+from __future__ import annotations
+
+import math
+import os
+import sys
+import time
+
+import numpy as np
+import scipy
+
+REF = "/root/reference/pkg/src"
+OUT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REF)
+
+import cfcent  # noqa: E402  (the reference)
+from cfcent import generators as gen  # noqa: E402
+from cfcent import resistance as res  # noqa: E402
+from cfcent import solver as slv  # noqa: E402
+
+sys.setrecursionlimit(20000)
+PROV = dict(numpy=np.__version__, scipy=scipy.__version__)
+
+
+def rcg(n, rng, p=0.15, weighted=False):
+    """Spanning tree plus Bernoulli extra edges (same recipe as the
+    reference test fixture pkg/tests/conftest.py:7-21)."""
+    us, vs = [], []
+    for v in range(1, n):
+        us.append(int(rng.integers(v)))
+        vs.append(v)
+    iu, iv = np.nonzero(np.triu(rng.random((n, n)) < p, 1))
+    us += iu.tolist()
+    vs += iv.tolist()
+    w = rng.uniform(0.2, 3.0, size=len(us)) if weighted else np.ones(len(us))
+    return cfcent.Graph.from_edges(np.asarray(us), np.asarray(vs), w, n=n)
+
+
+def level_summary(h):
+    kinds = np.array([{"elimination": 0, "aggregation": 1, "coarsest": 2}[l.kind.value]
+                      for l in h.levels], dtype=np.int64)
+    sizes = np.array([l.size for l in h.levels], dtype=np.int64)
+    nnz = np.array([l.matrix.nnz for l in h.levels], dtype=np.int64)
+    return kinds, sizes, nnz
+
+
+def save(name, **arrays):
+    path = os.path.join(OUT, name)
+    np.savez_compressed(path, **arrays, provenance=np.array(repr(PROV)))
+    print("wrote", path, os.path.getsize(path), "bytes")
+
+
+def small_graphs():
+    """Random small graphs: edges, hierarchy shape, solutions at tau=1e-10."""
+    rng = np.random.default_rng(20240601)
+    out = {}
+    for t in range(6):
+        n = int(rng.integers(30, 400))
+        g = rcg(n, rng, p=float(rng.uniform(0.02, 0.15)), weighted=bool(t % 2))
+        eu, ev, ew = g.edge_array()
+        cfg = slv.SolverConfig(tau=1e-10, max_direct_size=int(rng.integers(8, 40)))
+        h = slv.setup(cfcent.laplacian(g), cfg)
+        kinds, sizes, nnz = level_summary(h)
+        b = rng.standard_normal((5, n))
+        b -= b.mean(axis=1, keepdims=True)
+        pots = slv.solve_many(h, b)
+        x = np.stack([p.values for p in pots])
+        r = np.array([p.achieved_residual for p in pots])
+        first_agg = next((l.aggregates for l in h.levels if l.kind.value == "aggregation"),
+                         np.zeros(0, dtype=np.int64))
+        first_elim = next((l.f_nodes for l in h.levels if l.kind.value == "elimination"),
+                          np.zeros(0, dtype=np.int64))
+        out.update({f"g{t}_eu": eu, f"g{t}_ev": ev, f"g{t}_ew": ew, f"g{t}_n": np.int64(n),
+                    f"g{t}_mds": np.int64(cfg.max_direct_size),
+                    f"g{t}_kinds": kinds, f"g{t}_sizes": sizes, f"g{t}_nnz": nnz,
+                    f"g{t}_b": b, f"g{t}_x": x, f"g{t}_res": r,
+                    f"g{t}_agg0": first_agg, f"g{t}_elim0": first_elim})
+    out["count"] = np.int64(6)
+    save("small_graphs.npz", **out)
+
+
+def kats():
+    """Known answers from the reference's own unit tests, recomputed."""
+    P = gen.path_graph
+    d = {}
+    h = slv.setup(cfcent.laplacian(P(2)))
+    d["p2_solve"] = slv.solve(h, np.array([1.0, -1.0])).values
+    d["p3_r02"] = np.float64(res.effective_resistance(slv.setup(cfcent.laplacian(P(3))), 0, 2))
+    g = gen.complete_graph(3)
+    d["k3_r01"] = np.float64(res.effective_resistance(slv.setup(cfcent.laplacian(g)), 0, 1))
+    g = cfcent.Graph.from_edges([0, 1, 2], [1, 2, 3], [2.0, 4.0, 0.5])
+    d["wpath_r03"] = np.float64(res.effective_resistance(slv.setup(cfcent.laplacian(g)), 0, 3))
+    g = cfcent.Graph.from_edges([0, 0], [1, 1], [1.5, 0.5])
+    d["par_r01"] = np.float64(res.effective_resistance(slv.setup(cfcent.laplacian(g)), 0, 1))
+    g = gen.complete_graph(3)
+    h = slv.setup(cfcent.laplacian(g))
+    d["k3_exact"] = cfcent.cf_closeness_exact(g, h, [0, 1, 2]).vector([0, 1, 2])
+    g = P(3)
+    h = slv.setup(cfcent.laplacian(g))
+    d["p3_exact"] = cfcent.cf_closeness_exact(g, h, [0, 1, 2]).vector([0, 1, 2])
+    # star: one elimination level removes all leaves
+    h = slv.setup(cfcent.laplacian(gen.star_graph(100)), slv.SolverConfig(max_direct_size=10))
+    d["star_f"] = h.levels[0].f_nodes
+    d["star_sizes"] = np.array(h.level_sizes)
+    d["sketch_dims"] = np.array([res.sketch_dimension(2, 0.5), res.sketch_dimension(500, 0.2),
+                                 res.sketch_dimension(4096, math.sqrt(math.log(4096) / 63.5)),
+                                 res.sketch_dimension(2234040, 0.15)])
+    # PCG64 integers(0,2) sign stream, several shapes / seeds
+    for seed in (0, 5, 11):
+        d[f"bits_seed{seed}"] = np.random.default_rng(seed).integers(0, 2, size=(3, 777))
+    # pivot sets (config seeds)
+    d["piv_4096_64_0"] = cfcent.centrality.pivot_set(4096, 64, 0)
+    d["piv_1000_30_3"] = cfcent.centrality.pivot_set(1000, 30, 3)
+    save("kats.npz", **d)
+
+
+def config1():
+    """C1: grid 64x64; JL k=64 (seed 0) and sampling k=64 (seed 0), u=0."""
+    g = gen.grid_graph(64)
+    n = g.n
+    eps = math.sqrt(math.log(n) / 63.5)
+    d = {"eps": np.float64(eps)}
+    b_inc, w = cfcent.incidence_and_weights(g)
+    d["y_rows_0_3"] = None
+    # uncentred JL right-hand sides exactly as build_sketch forms them
+    st = b_inc.multiply(np.sqrt(w)[:, None]).T.tocsr()
+    rng = np.random.default_rng(0)
+    k = res.sketch_dimension(n, eps)
+    q = (rng.integers(0, 2, size=(k, g.m)).astype(np.float64) * 2.0 - 1.0) / math.sqrt(k)
+    y = (st @ q.T).T
+    d["y_rows_0_3"] = y[:4].copy()
+    d["y_sum_abs"] = np.abs(y).sum(axis=1)
+    query = [0, 1, 65, 2080, 4095]
+    d["query"] = np.array(query)
+    for tau in (1e-8, 1e-10):
+        cfg = slv.SolverConfig(tau=tau, seed=0)
+        h = slv.setup(cfcent.laplacian(g), cfg)
+        kinds, sizes, nnz = level_summary(h)
+        d["kinds"], d["sizes"], d["nnz"] = kinds, sizes, nnz
+        t0 = time.perf_counter()
+        jl = cfcent.cf_closeness_projection(g, h, query, eps, 0, cfg)
+        t1 = time.perf_counter()
+        sm = cfcent.cf_closeness_sampling(g, h, [0], 64, 0, cfg)
+        t2 = time.perf_counter()
+        tag = f"{tau:.0e}".replace("-", "m")
+        d[f"jl_{tag}"] = jl.vector(query)
+        d[f"samp_{tag}"] = sm.vector([0])
+        d[f"t_jl_{tag}"] = np.float64(t1 - t0)
+        d[f"t_samp_{tag}"] = np.float64(t2 - t1)
+        print("C1", tau, jl.vector(query), sm.vector([0]), t1 - t0, t2 - t1)
+    save("config1.npz", **d)
+
+
+def config2():
+    """C2: BA n=1e5, m0=4, seed 1; JL k=128 for 100 nodes (seed 2), Q seed 0."""
+    g = gen.barabasi_albert_graph(100000, 4, 1)
+    n = g.n
+    eps = math.sqrt(math.log(n) / 127.5)
+    query = np.sort(np.random.default_rng(2).choice(n, 100, replace=False))
+    d = {"eps": np.float64(eps), "query": query, "m": np.int64(g.m)}
+    for tau in (1e-6, 1e-10):
+        cfg = slv.SolverConfig(tau=tau, seed=0)
+        t0 = time.perf_counter()
+        h = slv.setup(cfcent.laplacian(g), cfg)
+        t1 = time.perf_counter()
+        kinds, sizes, nnz = level_summary(h)
+        d["kinds"], d["sizes"], d["nnz"] = kinds, sizes, nnz
+        jl = cfcent.cf_closeness_projection(g, h, query, eps, 0, cfg, threads=8)
+        t2 = time.perf_counter()
+        tag = f"{tau:.0e}".replace("-", "m")
+        d[f"jl_{tag}"] = jl.vector(query)
+        d[f"t_setup_{tag}"] = np.float64(t1 - t0)
+        d[f"t_jl_{tag}"] = np.float64(t2 - t1)
+        print("C2", tau, jl.vector(query)[:4], t1 - t0, t2 - t1)
+    save("config2.npz", **d)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["kats", "small", "c1", "c2"]
+    if "kats" in which:
+        kats()
+    if "small" in which:
+        small_graphs()
+    if "c1" in which:
+        config1()
+    if "c2" in which:
+        config2()

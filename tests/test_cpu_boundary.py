@@ -1,0 +1,145 @@
+"""CPU-side tests: the C-ABI library loads and exports every symbol declared
+in include/cfcent_b200.h; the host setup reproduces the reference's
+hierarchies (golden); API validation mirrors the reference."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_1607_02955_b200 as P
+from conftest import ROOT, golden, random_connected_graph_edges
+from paper_1607_02955_b200 import _native
+from paper_1607_02955_b200 import generators as G
+from paper_1607_02955_b200.solver import LevelKind, coarsen_aggregate, coarsen_eliminate, \
+    relaxed_test_vectors
+
+
+def header_symbols():
+    txt = open(os.path.join(ROOT, "include", "cfcent_b200.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(cf_\w+)\s*\(", txt, re.M)))
+
+
+def test_library_exports_header_symbols():
+    lib = _native.lib()
+    syms = header_symbols()
+    assert len(syms) >= 15
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(_native.exported_symbols())
+    assert lib.cf_version() == 1
+
+
+def test_no_device_here_is_loud():
+    if _native.device_available():
+        pytest.skip("a CUDA device is visible")
+    h = P.setup(P.laplacian(G.path_graph(4)))
+    with pytest.raises(RuntimeError):
+        P.solve(h, np.array([1.0, 0, 0, -1.0]))
+
+
+@pytest.mark.parametrize("t", range(6))
+def test_setup_matches_reference_hierarchy(t):
+    d = golden("small_graphs.npz")
+    g = P.Graph.from_edges(d[f"g{t}_eu"], d[f"g{t}_ev"], d[f"g{t}_ew"], n=int(d[f"g{t}_n"]))
+    h = P.setup(P.laplacian(g), P.SolverConfig(tau=1e-10, max_direct_size=int(d[f"g{t}_mds"])))
+    kinds = [{"elimination": 0, "aggregation": 1, "coarsest": 2}[l.kind.value] for l in h.levels]
+    assert kinds == d[f"g{t}_kinds"].tolist()
+    assert h.level_sizes == d[f"g{t}_sizes"].tolist()
+    assert [l.matrix.nnz for l in h.levels] == d[f"g{t}_nnz"].tolist()
+    agg = next((l.aggregates for l in h.levels if l.kind is LevelKind.AGGREGATION), np.zeros(0))
+    assert np.array_equal(agg, d[f"g{t}_agg0"])
+    f0 = next((l.f_nodes for l in h.levels if l.kind is LevelKind.ELIMINATION), np.zeros(0))
+    assert np.array_equal(f0, d[f"g{t}_elim0"])
+
+
+def test_setup_config1_matches_reference():
+    d = golden("config1.npz")
+    h = P.setup(P.laplacian(G.grid_graph(64)), P.SolverConfig(tau=1e-8))
+    assert h.level_sizes == d["sizes"].tolist()
+    assert [l.matrix.nnz for l in h.levels] == d["nnz"].tolist()
+
+
+def test_star_and_p2_shapes():
+    d = golden("kats.npz")
+    h = P.setup(P.laplacian(G.star_graph(100)), P.SolverConfig(max_direct_size=10))
+    assert h.levels[0].kind is LevelKind.ELIMINATION
+    assert np.array_equal(h.levels[0].f_nodes, d["star_f"])
+    assert h.level_sizes == d["star_sizes"].tolist()
+    h = P.setup(P.laplacian(G.path_graph(2)))
+    assert len(h.levels) == 1 and h.levels[0].kind is LevelKind.COARSEST
+
+
+def test_eliminate_and_aggregate_kats():
+    s, rec = coarsen_eliminate(P.laplacian(G.path_graph(3)).tocsr())
+    assert sorted(rec.f_nodes.tolist()) == [0, 2] and s.shape == (1, 1)
+    s, rec = coarsen_eliminate(P.laplacian(G.complete_graph(5)).tocsr(), degree_cap=4)
+    assert rec.f_nodes.size == 1 and s.shape == (4, 4)
+    lap = P.laplacian(G.complete_graph(7)).tocsr()
+    s, rec = coarsen_eliminate(lap, degree_cap=4)
+    assert rec is None and s is lap
+    us, vs = [], []
+    for blk in (0, 4):
+        for i in range(4):
+            for j in range(i + 1, 4):
+                us.append(blk + i)
+                vs.append(blk + j)
+    us.append(3)
+    vs.append(4)
+    lap = P.laplacian(P.Graph.from_edges(us, vs, n=8)).tocsr()
+    vec = relaxed_test_vectors(lap, 4, np.random.default_rng(0))
+    coarse, agg = coarsen_aggregate(lap, vec)
+    assert int(agg.max()) + 1 == 2 and coarse.toarray()[0, 1] < 0
+
+
+def test_validation_errors(rng):
+    import scipy.sparse as sp
+    with pytest.raises(P.DomainError):
+        P.setup(sp.eye(5, format="csr"))
+    lap = sp.block_diag([P.laplacian(G.path_graph(3))] * 2, format="csr")
+    with pytest.raises(P.DomainError):
+        P.setup(lap)
+    with pytest.raises(P.DomainError):
+        P.SolverConfig(tau=0.0)
+    with pytest.raises(P.DomainError):
+        P.SolverConfig(smoothing_steps=(0, 1))
+    with pytest.raises(P.DomainError):
+        P.SupplySpec(1, 1)
+    with pytest.raises(P.DomainError):
+        P.pivot_set(5, 6, 0)
+    g = G.path_graph(4)
+    h = P.setup(P.laplacian(g))
+    with pytest.raises(P.DomainError):
+        P.build_sketch(g, h, 1.5, 0)
+    with pytest.raises(P.DomainError):
+        P.solve(h, np.zeros(5))
+    with pytest.raises(P.DomainError):
+        P.cf_closeness_sampling(g, h, [], 2, 0)
+
+
+def test_graph_views(rng):
+    u, v, w = random_connected_graph_edges(50, rng, weighted=True)
+    g = P.Graph.from_edges(u, v, w, n=50)
+    b, wt = P.incidence_and_weights(g)
+    assert abs(b.T @ (b.multiply(wt[:, None])) - P.laplacian(g)).max() < 1e-12
+    from paper_1607_02955_b200.graph import edge_index_view
+    eid, sqw = edge_index_view(g)
+    eu, ev, _ = g.edge_array()
+    src = np.repeat(np.arange(g.n), np.diff(g.indptr))
+    assert np.array_equal(np.minimum(src, g.indices), eu[eid])
+    assert np.array_equal(np.maximum(src, g.indices), ev[eid])
+    for i in range(g.n):
+        seg = eid[g.indptr[i]:g.indptr[i + 1]]
+        assert np.all(np.diff(seg) > 0)  # ascending canonical id = the reference's sum order
+    gp = P.Graph.from_edges([0, 1, 1], [1, 0, 2], [2.0, 3.0, 1.0])
+    assert gp.m == 2 and gp.neighbors(0)[1].tolist() == [5.0]
+    lcc, mp = P.largest_connected_component(P.Graph.from_edges([0, 2], [1, 3], n=4))
+    assert lcc.n == 2 and mp == {0: 0, 1: 1}
+
+
+def test_generators_match_oracle():
+    from oracle import lamg_oracle as O
+    g = G.barabasi_albert_graph(3000, 4, 1)
+    og = O.barabasi_albert(3000, 4, 1)
+    assert np.array_equal(g.indptr, og[0]) and np.array_equal(g.indices, og[1])

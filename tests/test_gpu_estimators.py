@@ -1,0 +1,143 @@
+"""GPU parity tests of the estimator path: bit-exact seeded JL right-hand
+sides, closeness values vs the reference's golden values, the oracle and the
+exact pseudo-inverse (SURVEY.md §8(c) parity protocol)."""
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_1607_02955_b200 as P
+from conftest import dense_pinv_resistance, golden, random_connected_graph_edges
+from oracle import lamg_oracle as O
+from paper_1607_02955_b200 import generators as G
+from paper_1607_02955_b200.resistance import jl_rhs_rows
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("seed", [0, 1, 17])
+def test_jl_rhs_bit_exact_vs_oracle(seed, rng):
+    # odd edge count so rows start at odd half-word offsets too
+    u, v, w = random_connected_graph_edges(300, np.random.default_rng(seed), weighted=True)
+    g = P.Graph.from_edges(u, v, w, n=300)
+    og = O.graph_from_edges(u, v, w, n=300)
+    h = P.setup(P.laplacian(g))
+    for k in (1, 7, 64, 300):
+        ref, _ = O.jl_rhs(og, k, seed)
+        got = jl_rhs_rows(g, h, k, seed)
+        assert np.array_equal(got, ref), (k, np.abs(got - ref).max())
+    ref, _ = O.jl_rhs(og, 300, seed)
+    got = jl_rhs_rows(g, h, 300, seed, row0=37, rows=100)
+    assert np.array_equal(got, ref[37:137])
+
+
+def test_config1_rhs_golden():
+    d = golden("config1.npz")
+    g = G.grid_graph(64)
+    h = P.setup(P.laplacian(g))
+    got = jl_rhs_rows(g, h, 64, 0, rows=4)
+    assert np.array_equal(got, d["y_rows_0_3"])
+
+
+def test_config1_closeness_parity():
+    """C1: JL (k=64, seed 0) and sampling (64 pivots, seed 0) vs the reference
+    at tau 1e-8 (rel 1e-6) and both vs the exact pseudo-inverse."""
+    d = golden("config1.npz")
+    g = G.grid_graph(64)
+    eps = float(d["eps"])
+    q = d["query"]
+    for tau, tag in ((1e-8, "1em08"), (1e-10, "1em10")):
+        cfg = P.SolverConfig(tau=tau)
+        h = P.setup(P.laplacian(g), cfg)
+        jl = P.cf_closeness_projection(g, h, q, eps, 0, cfg)
+        assert jl.params["k"] == 64
+        assert np.allclose(jl.vector(q), d[f"jl_{tag}"], rtol=1e-6 if tau == 1e-8 else 1e-8)
+        sm = P.cf_closeness_sampling(g, h, [0], 64, 0, cfg)
+        assert np.allclose(sm.vector([0]), d[f"samp_{tag}"], rtol=1e-6 if tau == 1e-8 else 1e-8)
+        assert h.stats.max_residual <= tau
+    exact_jl = O.jl_exact_pinv(O.grid_graph(64), 64, 0, q)
+    cfg = P.SolverConfig(tau=1e-8)
+    h = P.setup(P.laplacian(g), cfg)
+    jl = P.cf_closeness_projection(g, h, q, eps, 0, cfg)
+    assert np.allclose(jl.vector(q), exact_jl, rtol=1e-6)
+
+
+def test_sketch_and_sums_match_oracle(rng):
+    u, v, w = random_connected_graph_edges(120, rng, weighted=True)
+    g = P.Graph.from_edges(u, v, w, n=120)
+    og = O.graph_from_edges(u, v, w, n=120)
+    cfg = P.SolverConfig(tau=1e-11)
+    h = P.setup(P.laplacian(g), cfg)
+    sk = P.build_sketch(g, h, 0.3, 5, cfg)
+    assert sk.k == O.sketch_rows(120, 0.3)
+    _, rhs = O.jl_rhs(og, sk.k, 5)
+    pinv = np.linalg.pinv(O.laplacian(og).toarray())
+    z_exact = rhs @ pinv
+    assert np.abs(sk.z - z_exact).max() <= 1e-8 * np.abs(z_exact).max()
+    assert np.abs(sk.z.mean(axis=1)).max() < 1e-10
+    sums = P.sketch_distance_sums(sk, [3, 50])
+    fused = P.cf_closeness_projection(g, h, [3, 50], 0.3, 5, cfg).vector([3, 50])
+    assert np.allclose((120 - 1) / sums, fused, rtol=1e-10)
+
+
+def test_resistance_kats():
+    d = golden("kats.npz")
+    h = P.setup(P.laplacian(G.path_graph(3)))
+    assert P.effective_resistance(h, 0, 2) == pytest.approx(2.0, rel=1e-6)
+    assert P.effective_resistance(h, 1, 1) == 0.0
+    h = P.setup(P.laplacian(G.complete_graph(3)))
+    assert P.effective_resistance(h, 0, 1) == pytest.approx(float(d["k3_r01"]), rel=1e-6)
+    g = P.Graph.from_edges([0, 1, 2], [1, 2, 3], [2.0, 4.0, 0.5])
+    h = P.setup(P.laplacian(g))
+    assert P.effective_resistance(h, 0, 3) == pytest.approx(2.75, rel=1e-6)
+    g = P.Graph.from_edges([0, 0], [1, 1], [1.5, 0.5])
+    h = P.setup(P.laplacian(g))
+    assert P.effective_resistance(h, 0, 1) == pytest.approx(0.5, rel=1e-8)
+    g = G.complete_graph(3)
+    h = P.setup(P.laplacian(g))
+    assert np.allclose(P.cf_closeness_exact(g, h, [0, 1, 2]).vector([0, 1, 2]), 1.5, rtol=1e-6)
+
+
+def test_sampling_and_exact_vs_pinv(rng):
+    u, v, w = random_connected_graph_edges(40, rng, weighted=True)
+    g = P.Graph.from_edges(u, v, w, n=40)
+    cfg = P.SolverConfig(tau=1e-10, max_direct_size=16)
+    h = P.setup(P.laplacian(g), cfg)
+    r = dense_pinv_resistance(P.laplacian(g).toarray())
+    exact = (40 - 1) / r.sum(axis=1)
+    got = P.cf_closeness_exact(g, h, range(40), cfg).vector(range(40))
+    assert np.allclose(got, exact, rtol=1e-7)
+    samp = P.cf_closeness_sampling(g, h, range(40), k=40, seed=5, config=cfg).vector(range(40))
+    assert np.allclose(samp, exact, rtol=1e-7)
+    piv = P.pivot_set(40, 9, 3)
+    s = P.cf_closeness_sampling(g, h, [0, 7], k=9, seed=3, config=cfg).vector([0, 7])
+    for v_, sv in zip([0, 7], s):
+        assert sv == pytest.approx((9 / 40) * 39 / r[v_, piv].sum(), rel=1e-7)
+
+
+def test_k1_own_pivot_undefined():
+    g = G.path_graph(3)
+    h = P.setup(P.laplacian(g))
+    piv = int(P.pivot_set(3, 1, 0)[0])
+    with pytest.raises(P.UndefinedScoreError):
+        P.cf_closeness_sampling(g, h, [piv], k=1, seed=0)
+
+
+@pytest.mark.slow
+def test_config2_closeness_parity():
+    """C2 (BA 1e5, JL k=128, 100 queries): vs the reference at tau_parity=1e-10
+    (both sides) within 1e-8, and at the config tau 1e-6 within 1e-6."""
+    d = golden("config2.npz")
+    g = G.barabasi_albert_graph(100000, 4, 1)
+    assert g.m == int(d["m"])
+    eps = float(d["eps"])
+    q = d["query"]
+    for tau, tag, tol in ((1e-10, "1em10", 1e-8), (1e-6, "1em06", 1e-6)):
+        cfg = P.SolverConfig(tau=tau)
+        h = P.setup(P.laplacian(g), cfg)
+        assert h.level_sizes == d["sizes"].tolist()
+        jl = P.cf_closeness_projection(g, h, q, eps, 0, cfg)
+        rel = np.abs(jl.vector(q) / d[f"jl_{tag}"] - 1).max()
+        assert rel <= tol, (tau, rel)
+        assert h.stats.max_residual <= tau

@@ -1,0 +1,160 @@
+"""GPU parity tests of the solve path (through the C-ABI) against the CPU
+oracle, the reference's golden vectors and the reference's known answers
+(pkg/tests/test_solver.py cases restated)."""
+
+import numpy as np
+import pytest
+
+import paper_1607_02955_b200 as P
+from conftest import dense_pinv_resistance, golden, random_connected_graph_edges
+from oracle import lamg_oracle as O
+from paper_1607_02955_b200 import generators as G
+
+pytestmark = pytest.mark.gpu
+
+
+def dense_solve(lap, b):
+    x = np.zeros(lap.shape[0])
+    x[1:] = np.linalg.solve(lap[1:, 1:], b[1:])
+    return x - x.mean()
+
+
+def test_p2_unit_supply():
+    h = P.setup(P.laplacian(G.path_graph(2)))
+    p = P.solve(h, np.array([1.0, -1.0]))
+    assert p.values == pytest.approx([0.5, -0.5], abs=1e-12)
+
+
+def test_zero_rhs_exact_zeros():
+    h = P.setup(P.laplacian(G.path_graph(5)))
+    p = P.solve(h, np.zeros(5))
+    assert np.all(p.values == 0.0) and p.achieved_residual == 0.0
+
+
+def test_grid_residual_contract(rng):
+    g = G.grid_graph(64)
+    h = P.setup(P.laplacian(g))
+    b = rng.standard_normal(g.n)
+    b -= b.mean()
+    p = P.solve(h, b)
+    lap = P.laplacian(g)
+    assert np.linalg.norm(b - lap @ p.values) / np.linalg.norm(b) <= 1e-5
+    assert abs(p.values.mean()) < 1e-12
+
+
+def test_unbalanced_rejected():
+    h = P.setup(P.laplacian(G.path_graph(4)))
+    with pytest.raises(P.DomainError):
+        P.solve(h, np.array([1.0, 0.0, 0.0, 0.0]))
+
+
+@pytest.mark.parametrize("t", range(6))
+def test_golden_small_graphs(t):
+    """Same hierarchy as the reference; solutions of the reference's supplies
+    agree with the reference's own solutions and the dense oracle."""
+    d = golden("small_graphs.npz")
+    g = P.Graph.from_edges(d[f"g{t}_eu"], d[f"g{t}_ev"], d[f"g{t}_ew"], n=int(d[f"g{t}_n"]))
+    cfg = P.SolverConfig(tau=1e-10, max_direct_size=int(d[f"g{t}_mds"]))
+    h = P.setup(P.laplacian(g), cfg)
+    assert h.level_sizes == d[f"g{t}_sizes"].tolist()
+    pots = P.solve_many(h, d[f"g{t}_b"])
+    x = np.stack([p.values for p in pots])
+    ref = d[f"g{t}_x"]
+    lap = P.laplacian(g).toarray()
+    exact = np.stack([dense_solve(lap, b) for b in d[f"g{t}_b"]])
+    scale = np.abs(exact).max()
+    assert np.abs(x - ref).max() <= 1e-7 * scale
+    assert np.abs(x - exact).max() <= 1e-7 * scale
+    assert max(p.achieved_residual for p in pots) <= 1e-10
+
+
+def test_matches_dense_oracle_random(rng):
+    for _ in range(8):
+        n = int(rng.integers(3, 40))
+        u, v, w = random_connected_graph_edges(n, rng, weighted=True)
+        g = P.Graph.from_edges(u, v, w, n=n)
+        h = P.setup(P.laplacian(g), P.SolverConfig(tau=1e-10, max_direct_size=2))
+        b = rng.standard_normal(n)
+        b -= b.mean()
+        p = P.solve(h, b)
+        exp = dense_solve(P.laplacian(g).toarray(), b)
+        assert p.values == pytest.approx(exp, abs=1e-7 * max(1, np.abs(exp).max()))
+
+
+def test_determinism_columns_negation_batch(rng):
+    g = G.grid_graph(16)
+    h = P.setup(P.laplacian(g))
+    b = rng.standard_normal(g.n)
+    b -= b.mean()
+    r = P.solve_many(h, [b, b, -b])
+    assert np.array_equal(r[0].values, r[1].values)
+    assert np.array_equal(r[0].values, -r[2].values)
+    others = rng.standard_normal((70, g.n))
+    others -= others.mean(axis=1, keepdims=True)
+    alone = P.solve_many(h, [b])[0]
+    grouped = P.solve_many(h, np.vstack([others, b[None, :]]))[-1]
+    # per-column independence on the device: bitwise, stronger than the
+    # reference's 1e-12 (pkg/tests/test_solver.py:273-285)
+    assert np.array_equal(alone.values, grouped.values)
+    t1 = P.solve_many(h, others, threads=1)
+    t4 = P.solve_many(h, others, threads=4)
+    assert all(np.array_equal(a.values, c.values) for a, c in zip(t1, t4))
+
+
+def test_many_rhs_random_graph(rng):
+    u, v, w = random_connected_graph_edges(1000, rng)
+    g = P.Graph.from_edges(u, v, w, n=1000)
+    h = P.setup(P.laplacian(g))
+    lap = P.laplacian(g)
+    s = rng.standard_normal((300, g.n))
+    s -= s.mean(axis=1, keepdims=True)
+    for pot, b in zip(P.solve_many(h, s), s):
+        assert np.linalg.norm(b - lap @ pot.values) / np.linalg.norm(b) <= 1e-5
+
+
+def test_fallback_rescues_starved_multigrid(rng):
+    g = G.grid_graph(20)
+    cfg = P.SolverConfig(max_cycles=1, smoothing_steps=(1, 1), max_direct_size=2)
+    h = P.setup(P.laplacian(g), cfg)
+    b = rng.standard_normal(g.n)
+    b -= b.mean()
+    p = P.solve(h, b, cfg)
+    assert np.linalg.norm(b - P.laplacian(g) @ p.values) / np.linalg.norm(b) <= 1e-5
+    assert h.stats.fallback_solves >= 1
+
+
+def test_unreachable_tolerance_raises(rng):
+    cfg = P.SolverConfig(tau=1e-300, max_cycles=8)
+    h = P.setup(P.laplacian(G.path_graph(30)), cfg)
+    b = rng.standard_normal(30)
+    b -= b.mean()
+    with pytest.raises(P.ConvergenceError) as err:
+        P.solve(h, b, cfg)
+    assert 0 < err.value.best_residual < 1e-10
+
+
+def test_block_widths_agree(rng):
+    """Every device block width computes each column identically."""
+    g = G.grid_graph(12)
+    h = P.setup(P.laplacian(g))
+    s = rng.standard_normal((200, g.n))
+    s -= s.mean(axis=1, keepdims=True)
+    full = np.stack([p.values for p in P.solve_many(h, s)])
+    for cnt in (1, 5, 9, 17, 33, 65, 129):
+        part = np.stack([p.values for p in P.solve_many(h, s[:cnt])])
+        assert np.array_equal(part, full[:cnt]), cnt
+
+
+def test_vs_oracle_bigger(rng):
+    """BA 20k: device solutions vs the oracle's reference-algorithm solutions."""
+    g = G.barabasi_albert_graph(20000, 4, 7)
+    og = O.barabasi_albert(20000, 4, 7)
+    cfg = P.SolverConfig(tau=1e-10)
+    h = P.setup(P.laplacian(g), cfg)
+    oh = O.build_hierarchy(O.laplacian(og), O.OracleConfig(tau=1e-10))
+    assert h.level_sizes == [l["A"].shape[0] for l in oh["levels"]]
+    b = rng.standard_normal((40, g.n))
+    b -= b.mean(axis=1, keepdims=True)
+    x = np.stack([p.values for p in P.solve_many(h, b)])
+    ref, _ = O.solve_rows(oh, b)
+    assert np.abs(x - ref).max() <= 1e-8 * np.abs(ref).max()
