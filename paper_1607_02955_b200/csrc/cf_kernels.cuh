@@ -20,12 +20,16 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kRowsPerPart = 256;
 
+// One row group per warp for every width: the row -> (warp, pass) mapping and
+// hence every reduction order is identical for all KC, so a column's result
+// does not depend on the width of the block it was solved in.  For KC < 32
+// only the first KC lanes work (narrow blocks are latency-bound anyway).
 template <int KC>
 struct Lay {
-    static constexpr int LPR = KC < 32 ? KC : 32;  // lanes per row group
+    static constexpr int LPR = KC < 32 ? KC : 32;  // working lanes per row group
     static constexpr int VEC = KC / LPR;           // doubles per lane
-    static constexpr int RPW = 32 / LPR;           // row groups per warp
-    static constexpr int RPB = RPW * kWarps;       // row groups per CTA pass
+    static constexpr int RPW = 1;                  // row groups per warp
+    static constexpr int RPB = kWarps;             // row groups per CTA pass
 };
 
 template <int V>
@@ -135,12 +139,15 @@ __device__ __forceinline__ void cta_reduce_store(DV<Lay<KC>::VEC> (&loc)[NQ], do
                                                  int64_t part) {
     using L = Lay<KC>;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int slot = warp * L::RPW + lane / L::LPR;
-    const int c0 = (lane % L::LPR) * L::VEC;
+    const int slot = warp;
+    const int c0 = lane * L::VEC;
+    if (lane < L::LPR) {
 #pragma unroll
-    for (int q = 0; q < NQ; ++q)
+        for (int q = 0; q < NQ; ++q)
 #pragma unroll
-        for (int t = 0; t < L::VEC; ++t) smem[((size_t)q * L::RPB + slot) * KC + c0 + t] = loc[q].v[t];
+            for (int t = 0; t < L::VEC; ++t)
+                smem[((size_t)q * L::RPB + slot) * KC + c0 + t] = loc[q].v[t];
+    }
     __syncthreads();
     for (int idx = threadIdx.x; idx < NQ * KC; idx += blockDim.x) {
         int q = idx / KC, c = idx % KC;

@@ -38,10 +38,12 @@ enum ColState { COL_ZERO = 0, COL_ACTIVE = 1, COL_CONV = 2, COL_FALLBACK = 3 };
     using Lt = Lay<KC>;                                       \
     constexpr int V = Lt::VEC;                                \
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5; \
-    const int slot = warp * Lt::RPW + lane / Lt::LPR;         \
-    const int c0 = (lane % Lt::LPR) * V;                      \
+    const int slot = warp;                                    \
+    const bool lane_ok = lane < Lt::LPR;                      \
+    const int c0 = (lane_ok ? lane : 0) * V;                  \
     (void)slot;                                               \
-    (void)c0;
+    (void)c0;                                                 \
+    (void)lane_ok;
 
 // R = B - L X ; partials of sum(R), sum(R^2)  (solver.py:694-695)
 template <int KC>
@@ -62,7 +64,7 @@ __global__ void __launch_bounds__(kThreads) k_residual(int n, const int64_t* __r
     const int64_t part = blockIdx.x;
     for (int r = slot; r < kRowsPerPart; r += Lt::RPB) {
         int64_t i = part * kRowsPerPart + r;
-        if (i >= n) break;
+        if (i >= n || !lane_ok) break;
         DV<V> acc;
         zero(acc);
         gather_row<KC, false>(col, val, rp[i], rp[i + 1], nullptr, X, c0, acc);
@@ -91,7 +93,7 @@ __global__ void __launch_bounds__(kThreads) k_spmm(int n, const int64_t* __restr
                                                    double* __restrict__ Y) {
     CF_LANE_SETUP(KC)
     int64_t i = (int64_t)blockIdx.x * Lt::RPB + slot;
-    if (i >= n) return;
+    if (i >= n || !lane_ok) return;
     DV<V> acc;
     zero(acc);
     gather_row<KC, false>(col, val, rp[i], rp[i + 1], nullptr, X, c0, acc);
@@ -116,7 +118,7 @@ __global__ void __launch_bounds__(kThreads) k_colstats(int n, const double* __re
     const int64_t part = blockIdx.x;
     for (int r = slot; r < kRowsPerPart; r += Lt::RPB) {
         int64_t i = part * kRowsPerPart + r;
-        if (i >= n) break;
+        if (i >= n || !lane_ok) break;
         DV<V> b = ldv<V>(B + i * KC + c0);
 #pragma unroll
         for (int t = 0; t < V; ++t) {
@@ -143,7 +145,7 @@ __global__ void __launch_bounds__(kThreads) k_dot2(int n, const double* __restri
     const int64_t part = blockIdx.x;
     for (int r = slot; r < kRowsPerPart; r += Lt::RPB) {
         int64_t i = part * kRowsPerPart + r;
-        if (i >= n) break;
+        if (i >= n || !lane_ok) break;
         DV<V> a = ldv<V>(U1 + i * KC + c0), b = ldv<V>(V1 + i * KC + c0);
         DV<V> c = ldv<V>(U2 + i * KC + c0), d = ldv<V>(V2 + i * KC + c0);
 #pragma unroll
@@ -168,7 +170,7 @@ __global__ void __launch_bounds__(kThreads) k_colsum(int n, const double* __rest
     const int64_t part = blockIdx.x;
     for (int r = slot; r < kRowsPerPart; r += Lt::RPB) {
         int64_t i = part * kRowsPerPart + r;
-        if (i >= n) break;
+        if (i >= n || !lane_ok) break;
         DV<V> x = ldv<V>(X + i * KC + c0);
         if (Y) {
             DV<V> y = ldv<V>(Y + i * KC + c0);
@@ -181,25 +183,29 @@ __global__ void __launch_bounds__(kThreads) k_colsum(int n, const double* __rest
     cta_reduce_store<KC, 1>(loc, smem, parts, nparts, part);
 }
 
-// out[q*KC + c] = sum_p parts[q*qstride + p*KC + c]  (fixed order)
+// out[q*KC + c] = sum_p parts[q*qstride + p*KC + c] in a canonical order that
+// depends on nparts only: 8 contiguous segments summed left to right, then the
+// segment sums in order.
+constexpr int kFinSeg = 8;
 template <int KC>
 __global__ void __launch_bounds__(kThreads) k_finalize(const double* __restrict__ parts,
                                                        int64_t nparts, int64_t qstride,
                                                        double* __restrict__ out) {
-    constexpr int NSEG = kThreads / KC;
-    __shared__ double sm[kThreads];
+    __shared__ double sm[kFinSeg * KC];
     const int q = blockIdx.x;
-    const int c = threadIdx.x % KC, seg = threadIdx.x / KC;
     const double* p0 = parts + (size_t)q * qstride;
-    int64_t per = (nparts + NSEG - 1) / NSEG;
-    int64_t beg = seg * per, end = min(nparts, beg + per);
-    double s = 0.0;
-    for (int64_t p = beg; p < end; ++p) s += p0[p * KC + c];
-    sm[threadIdx.x] = s;
+    const int64_t per = (nparts + kFinSeg - 1) / kFinSeg;
+    for (int task = threadIdx.x; task < kFinSeg * KC; task += blockDim.x) {
+        const int c = task % KC, seg = task / KC;
+        const int64_t beg = seg * per, end = min(nparts, beg + per);
+        double s = 0.0;
+        for (int64_t p = beg; p < end; ++p) s += p0[p * KC + c];
+        sm[task] = s;
+    }
     __syncthreads();
-    if (threadIdx.x < KC) {
+    for (int c = threadIdx.x; c < KC; c += blockDim.x) {
         double t = 0.0;
-        for (int g = 0; g < NSEG; ++g) t += sm[g * KC + c];
+        for (int g = 0; g < kFinSeg; ++g) t += sm[g * KC + c];
         out[q * KC + c] = t;
     }
 }
@@ -246,7 +252,7 @@ __global__ void __launch_bounds__(kThreads) k_center(int n, double* __restrict__
                                                      const double* __restrict__ mean) {
     CF_LANE_SETUP(KC)
     int64_t i = (int64_t)blockIdx.x * Lt::RPB + slot;
-    if (i >= n) return;
+    if (i >= n || !lane_ok) return;
     DV<V> r = ldv_c<V>(R + i * KC + c0);
 #pragma unroll
     for (int t = 0; t < V; ++t) r.v[t] = r.v[t] - mean[c0 + t];
@@ -261,7 +267,7 @@ __global__ void __launch_bounds__(kThreads) k_update(int n, double* __restrict__
                                                      const int* __restrict__ state) {
     CF_LANE_SETUP(KC)
     int64_t i = (int64_t)blockIdx.x * Lt::RPB + slot;
-    if (i >= n) return;
+    if (i >= n || !lane_ok) return;
     DV<V> x = ldv_c<V>(X + i * KC + c0), c = ldv<V>(C + i * KC + c0);
 #pragma unroll
     for (int t = 0; t < V; ++t)
@@ -277,7 +283,7 @@ __global__ void __launch_bounds__(kThreads) k_lincomb(int n, double* __restrict_
                                                       const double* __restrict__ coef) {
     CF_LANE_SETUP(KC)
     int64_t i = (int64_t)blockIdx.x * Lt::RPB + slot;
-    if (i >= n) return;
+    if (i >= n || !lane_ok) return;
     DV<V> y = ldv_c<V>(Y + i * KC + c0);
     DV<V> u, w;
     if (U) u = ldv_c<V>(U + i * KC + c0); else zero(u);
@@ -285,7 +291,7 @@ __global__ void __launch_bounds__(kThreads) k_lincomb(int n, double* __restrict_
 #pragma unroll
     for (int t = 0; t < V; ++t) {
         int c = c0 + t;
-        y.v[t] = coef[c] * y.v[t] + coef[KC + c] * u.v[t] + coef[2 * KC + c] * w.v[t];
+        y.v[t] = fma(coef[c], y.v[t], fma(coef[KC + c], u.v[t], coef[2 * KC + c] * w.v[t]));
     }
     stv<V>(Y + i * KC + c0, y);
 }
@@ -304,7 +310,7 @@ __global__ void __launch_bounds__(kThreads) k_gs(const int32_t* __restrict__ row
                                                  double* __restrict__ X, int from_zero) {
     CF_LANE_SETUP(KC)
     int64_t g = (int64_t)blockIdx.x * Lt::RPB + slot;
-    if (g >= cnt) return;
+    if (g >= cnt || !lane_ok) return;
     int64_t i = rows[g];
     DV<V> acc;
     zero(acc);
@@ -325,7 +331,7 @@ __global__ void __launch_bounds__(kThreads) k_agg_restrict(
     const double* __restrict__ B, const double* __restrict__ X, double* __restrict__ Bc) {
     CF_LANE_SETUP(KC)
     int64_t a = (int64_t)blockIdx.x * Lt::RPB + slot;
-    if (a >= nc) return;
+    if (a >= nc || !lane_ok) return;
     DV<V> out;
     zero(out);
     for (int q = aptr[a]; q < aptr[a + 1]; ++q) {
@@ -358,7 +364,7 @@ __global__ void __launch_bounds__(kThreads) k_agg_ls(
         const int64_t part = blockIdx.x;
         for (int r = slot; r < kRowsPerPart; r += Lt::RPB) {
             int64_t i = part * kRowsPerPart + r;
-            if (i >= n) break;
+            if (i >= n || !lane_ok) break;
             DV<V> acc;
             zero(acc);
             gather_row<KC, true>(col, val, rp[i], rp[i + 1], agg, Xc, c0, acc);
@@ -375,7 +381,7 @@ __global__ void __launch_bounds__(kThreads) k_agg_ls(
         const int64_t part = blockIdx.x - pf;
         for (int r = slot; r < kRowsPerPart; r += Lt::RPB) {
             int64_t a = part * kRowsPerPart + r;
-            if (a >= nc) break;
+            if (a >= nc || !lane_ok) break;
             DV<V> b = ldv<V>(Bc + a * KC + c0), x = ldv<V>(Xc + a * KC + c0);
 #pragma unroll
             for (int t = 0; t < V; ++t) loc[0].v[t] = fma(b.v[t], x.v[t], loc[0].v[t]);
@@ -392,7 +398,7 @@ __global__ void __launch_bounds__(kThreads) k_agg_correct(int n, const int32_t* 
                                                           const double* __restrict__ ls) {
     CF_LANE_SETUP(KC)
     int64_t i = (int64_t)blockIdx.x * Lt::RPB + slot;
-    if (i >= n) return;
+    if (i >= n || !lane_ok) return;
     DV<V> x = ldv_c<V>(X + i * KC + c0);
     DV<V> d = ldv<V>(Xc + (size_t)agg[i] * KC + c0);
 #pragma unroll
@@ -413,7 +419,7 @@ __global__ void __launch_bounds__(kThreads) k_elim_restrict(
     const double* __restrict__ B, double* __restrict__ Bc) {
     CF_LANE_SETUP(KC)
     int64_t i = (int64_t)blockIdx.x * Lt::RPB + slot;
-    if (i >= nc) return;
+    if (i >= nc || !lane_ok) return;
     DV<V> acc;
     zero(acc);
     for (int64_t p = wp[i]; p < wp[i + 1]; ++p) {
@@ -438,6 +444,7 @@ __global__ void __launch_bounds__(kThreads) k_elim_interp(
     const double* __restrict__ B, const double* __restrict__ Xc, double* __restrict__ X) {
     CF_LANE_SETUP(KC)
     int64_t g = (int64_t)blockIdx.x * Lt::RPB + slot;
+    if (!lane_ok) return;
     if (g < nc) {
         DV<V> x = ldv<V>(Xc + g * KC + c0);
         stv<V>(X + (size_t)cn[g] * KC + c0, x);
@@ -463,7 +470,7 @@ __global__ void __launch_bounds__(kThreads) k_dense(int n, const double* __restr
                                                     double* __restrict__ X) {
     CF_LANE_SETUP(KC)
     int64_t i = (int64_t)blockIdx.x * Lt::RPB + slot;
-    if (i >= n) return;
+    if (i >= n || !lane_ok) return;
     DV<V> acc;
     zero(acc);
     const double* m = M + (size_t)i * n;
@@ -824,7 +831,7 @@ __global__ void __launch_bounds__(kThreads) k_diag_scale(int n, const double* __
                                                          double* __restrict__ Z) {
     CF_LANE_SETUP(KC)
     int64_t i = (int64_t)blockIdx.x * Lt::RPB + slot;
-    if (i >= n) return;
+    if (i >= n || !lane_ok) return;
     DV<V> r = ldv_c<V>(R + i * KC + c0);
     double dinv = 1.0 / fmax(diag[i], 2.2250738585072014e-308);
 #pragma unroll
@@ -838,7 +845,7 @@ __global__ void __launch_bounds__(kThreads) k_addc(int n, double* __restrict__ X
                                                    const double* __restrict__ coef) {
     CF_LANE_SETUP(KC)
     int64_t i = (int64_t)blockIdx.x * Lt::RPB + slot;
-    if (i >= n) return;
+    if (i >= n || !lane_ok) return;
     DV<V> x = ldv_c<V>(X + i * KC + c0);
 #pragma unroll
     for (int t = 0; t < V; ++t) x.v[t] = x.v[t] + coef[KC + c0 + t];

@@ -156,9 +156,6 @@ def sketch_dimension(n: int, epsilon: float) -> int:
     return max(1, math.ceil(math.log(n) / epsilon ** 2))
 
 
-_GRAPH_CACHE: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
-
-
 class _DeviceGraph:
     """Adjacency + canonical edge ids + sqrt(w) on the device (one per
     (graph, hierarchy) pair)."""
@@ -186,7 +183,7 @@ class _DeviceGraph:
 
 
 def _device_graph(g: Graph, hierarchy: MultigridHierarchy) -> _DeviceGraph:
-    per = _GRAPH_CACHE.setdefault(hierarchy, {})
+    per = hierarchy._graphs
     key = id(g)
     ent = per.get(key)
     if ent is None or ent[0]() is not g:

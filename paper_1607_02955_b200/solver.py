@@ -226,6 +226,7 @@ class MultigridHierarchy:
     _dev: _DeviceHierarchy | None = field(default=None, repr=False, compare=False)
     _dev_lock: threading.Lock = field(default_factory=threading.Lock, repr=False,
                                       compare=False)
+    _graphs: dict = field(default_factory=dict, repr=False, compare=False)
 
     @property
     def n(self) -> int:
