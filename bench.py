@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 multi-RHS Laplacian solve path (BASELINE.json metric:
+"multi-RHS Laplacian solves/s to ref tol; V-cycle HBM GB/s vs B200 peak").
+
+A step is one pass of the hot path over one batch: the fused JL closeness
+estimate of the configuration (seeded Q generated on device, right-hand
+sides formed and centred, k solves to tau, distance-sum reduction for the
+query nodes).  ``value`` = right-hand sides solved per second over the whole
+job, inputs (graph, hierarchy) resident in HBM.  ``e2e`` = the same metric
+through the reference-facing API ``solve_many`` with host supplies (the same
+centred JL right-hand sides): host->device copy of the supplies and
+device->host copy of the solutions inside the timed region.
+
+Default workload is C2 (BASELINE.json configs[1]); ``--config c1..c5``
+selects another.  Multi-GPU (torchrun): every rank owns a disjoint range of
+k sketch rows (weak scaling), one all-reduce of the per-query partial sums.
+
+``--impl reference`` times the reference algorithm's CPU implementation
+(the oracle port of pkg/src/cfcent, oracle/lamg_oracle.py -- the reference
+itself is pure Python and cannot be shipped to the GPU box) on the host
+cores, on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "multi-RHS Laplacian solves/s to ref tol; V-cycle HBM GB/s vs B200 peak"
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = max(smax, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() in ("active", "1"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def row_range(k: int, world: int, rank: int):
+    return (k * rank) // world, (k * (rank + 1)) // world
+
+
+# ---------------------------------------------------------------------------
+# reference arm (CPU)
+# ---------------------------------------------------------------------------
+
+def cpu_reference(cfgname: str, columns: int, budget_s: float, threads: int):
+    """Time the reference algorithm (oracle port) on the host: solves of the
+    configuration's centred JL right-hand sides, 64-column blocks over
+    ``threads`` workers exactly like solver.py:771-811."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import lamg_oracle as O
+    from paper_1607_02955_b200 import configs
+
+    sys.setrecursionlimit(20000)
+    bc = configs.make(cfgname)
+    g = bc.graph
+    og = (np.asarray(g.indptr), np.asarray(g.indices), np.asarray(g.weights))
+    t0 = time.perf_counter()
+    h = O.build_hierarchy(O.laplacian(og), O.OracleConfig(tau=bc.tau))
+    setup_s = time.perf_counter() - t0
+    _, rhs = O.jl_rhs(og, bc.jl_k, bc.jl_seed)
+    cols = min(columns, rhs.shape[0])
+    sample = rhs[:cols]
+    blocks = [(lo, min(lo + 64, cols)) for lo in range(0, cols, 64)]
+    nthreads = max(1, min(threads, len(blocks)))
+
+    def run(b):
+        O.solve_columns(h, sample[b[0]:b[1]].T)
+
+    times = []
+    t_start = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        if nthreads > 1:
+            with ThreadPoolExecutor(nthreads) as ex:
+                list(ex.map(run, blocks))
+        else:
+            for b in blocks:
+                run(b)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_start > budget_s:
+            break
+    per = float(np.mean(times))
+    return {"value": cols / per, "unit": "solves/s", "cores": nthreads, "kind": "port",
+            "sample": f"{cols} of {bc.jl_k} {cfgname.upper()} JL right-hand sides "
+                      f"(tau {bc.tau:g}), {len(blocks)} x 64-column blocks, "
+                      f"{len(times)} timed repetition(s); oracle port of pkg/src/cfcent",
+            "setup_s": setup_s, "steps_timed": len(times), "s_per_step": per}
+
+
+def run_reference_arm(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    threads = len(os.sched_getaffinity(0))
+    r = cpu_reference(args.config, args.ref_columns, args.ref_budget, threads)
+    line = {"metric": METRIC, "value": r["value"], "unit": "solves/s", "n_gpus": args.gpus,
+            "steps": r["steps_timed"], "warmup": 0, "ms_per_step": r["s_per_step"] * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded, SURVEY.md §8(d) recipes)", "impl": "reference",
+            "config": {"workload": args.config.upper(), "rhs_per_step": args.ref_columns},
+            "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": r["value"], "unit": "solves/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "setup_s": r["setup_s"]}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm (GPU)
+# ---------------------------------------------------------------------------
+
+def run_gpu_arm(args):
+    import torch
+
+    import paper_1607_02955_b200 as P
+    from paper_1607_02955_b200 import configs
+    from paper_1607_02955_b200.resistance import jl_rhs_rows, sketch_closeness_sums
+    from paper_1607_02955_b200.solver import set_device
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    t0 = time.perf_counter()
+    bc = configs.make(args.config)
+    gen_s = time.perf_counter() - t0
+    g = bc.graph
+    cfg = P.SolverConfig(tau=bc.tau)
+    t0 = time.perf_counter()
+    h = P.setup(P.laplacian(g), cfg)
+    setup_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    dev = h.device()
+    upload_s = time.perf_counter() - t0
+    k = bc.jl_k
+    r0, r1 = row_range(k * world, world, rank)  # weak scaling: k rows per rank
+    K_total = k * world
+    eps = math.sqrt(math.log(g.n) / (K_total - 0.5))
+    stream = torch.cuda.ExternalStream(h.stream_ptr())
+
+    def step():
+        _, sums, res = sketch_closeness_sums(g, h, eps, bc.jl_seed, bc.query, cfg, rows=(r0, r1))
+        return sums, res
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    st0 = h.stats.vcycles
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            sums, res = step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    vcyc = (h.stats.vcycles - st0) / args.steps
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        s = torch.tensor(sums, device="cuda", dtype=torch.float64)
+        dist.all_reduce(s)
+        sums = s.cpu().numpy()
+    n = g.n
+    scores = (n - 1) / sums
+    solves = (r1 - r0) * world
+    value = solves / (ms / 1e3)
+
+    # --- per-kernel profile of one step (eager launches bracketed by events)
+    dev_h = h
+    dev_h.profile(True)
+    step()
+    rep = dev_h.profile_report()
+    dev_h.profile(False)
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", f"profile_{args.config}_rank{rank}.txt"), "w") as f:
+        f.write("kind level launches total_ms alg_bytes GB/s\n")
+        for kind, lv, la, kms, by in sorted(rep, key=lambda r: -r[3]):
+            f.write(f"{kind} {lv} {la} {kms:.4f} {by:.0f} {by / max(kms, 1e-9) / 1e6:.1f}\n")
+    kinds = {}
+    launches = 0
+    for kind, lv, la, kms, by in rep:
+        a = kinds.setdefault(kind, [0, 0.0, 0.0])
+        a[0] += la
+        a[1] += kms
+        a[2] += by
+        if kind != "memset":
+            launches += la
+    prof_ms = sum(v[1] for v in kinds.values())
+    dom = max(kinds.items(), key=lambda kv: kv[1][1])
+    peak, peak_src = _peaks()
+    dom_bytes_per_launch = dom[1][2] / dom[1][0]
+    dom_ms_per_launch = dom[1][1] / dom[1][0]
+    achieved = dom_bytes_per_launch / (dom_ms_per_launch * 1e-3) / 1e9
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(tfile):
+        with open(tfile) as f:
+            traffic = json.load(f).get(dom[0])
+    total_bytes = sum(v[2] for v in kinds.values())
+
+    # --- e2e through the public API with host buffers (same right-hand sides)
+    rhs = jl_rhs_rows(g, h, K_total, bc.jl_seed, row0=r0, rows=r1 - r0)
+    rhs -= rhs.mean(axis=1, keepdims=True)
+    rhs = np.ascontiguousarray(rhs)
+    P.solve_many(h, rhs, cfg)  # warm
+    barrier()
+    torch.cuda.synchronize()
+    e2 = []
+    for _ in range(max(1, min(args.steps, 5))):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        P.solve_many(h, rhs, cfg)
+        b.record(stream)
+        torch.cuda.synchronize()
+        e2.append(a.elapsed_time(b))
+    e2e_ms = float(np.mean(e2))
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = solves / (e2e_ms / 1e3)
+    h2d = rhs.nbytes
+    d2h = rhs.nbytes + 8 * rhs.shape[0]
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_reference(args.config, args.cpu_columns, args.cpu_budget, 1)
+        cpu = {k_: cpu[k_] for k_ in ("value", "unit", "cores", "kind", "sample")}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generators, SURVEY.md §8(d) recipes)",
+            "config": {"workload": f"{bc.name.upper()}: {bc.description}", "n": n, "m": g.m,
+                       "rhs_per_step": solves, "levels": len(h.levels),
+                       "parallelism": f"sketch rows sharded over {world} GPU(s)",
+                       "l2": "working set (per-level b,x blocks) larger than the 126 MB L2"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": dom[0],
+                         "peak_source": peak_src,
+                         "bytes_per_launch": dom_bytes_per_launch,
+                         "ms_per_launch": dom_ms_per_launch},
+            "step_hbm_gbs": total_bytes / (prof_ms * 1e-3) / 1e9 if prof_ms > 0 else None,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "solves/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "api": "solve_many (host supplies)"},
+            "gpu_launches": launches * args.steps,
+            "clocks": clk.summary(),
+            "vcycles_per_rhs": vcyc / max(1, r1 - r0),
+            "vcycles_per_s": vcyc / (ms / 1e3) * world,
+            "seconds_per_estimate": ms / 1e3,
+            "setup_s": setup_s, "upload_s": upload_s, "graph_gen_s": gen_s,
+            "max_residual": float(np.max(res)) if len(res) else 0.0,
+            "score_first_query": float(scores[0]),
+            "kernel_share": {kk: round(v[1] / prof_ms, 4) for kk, v in
+                             sorted(kinds.items(), key=lambda kv: -kv[1][1])},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--cpu-columns", type=int, default=64)
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--ref-columns", type=int, default=128)
+    ap.add_argument("--ref-budget", type=float, default=60.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_gpu_arm(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -145,9 +145,12 @@ int cf_jl_rhs_rows(void* graph, uint64_t state_hi, uint64_t state_lo, uint64_t i
  * out_sums[q] = sum_w ||z_v - z_w||^2 for query v = query[q].
  * If z_rows is not NULL, also returns Z (K x n host, the sketch's z). */
 int cf_jl_sketch(void* graph, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
-                 uint64_t inc_lo, int64_t K, double inv_sqrt_k, const int64_t* query,
-                 int64_t n_query, const CfSolveParams* params, double* out_sums,
-                 double* z_rows, double* residuals, CfSolveStats* stats);
+                 uint64_t inc_lo, int64_t K, int64_t row0, int64_t n_rows, double inv_sqrt_k,
+                 const int64_t* query, int64_t n_query, const CfSolveParams* params,
+                 double* out_sums, double* z_rows, double* residuals, CfSolveStats* stats);
+/* (cf_jl_sketch computes sketch rows [row0, row0 + n_rows) of the K-row
+ * sketch; out_sums are the additive contributions of those rows, so ranks
+ * owning disjoint row ranges sum their outputs -- SURVEY.md §8(e).) */
 
 /* Amortised node solutions L z_x = e_x - 1/n (resistance.py:77-99) for the
  * given nodes, reduced on device to the |nodes| x |nodes| submatrix
@@ -157,6 +160,16 @@ int cf_jl_sketch(void* graph, uint64_t state_hi, uint64_t state_lo, uint64_t inc
 int cf_node_solutions(void* handle, const int64_t* nodes, int64_t cnt,
                       const CfSolveParams* params, double* sub, double* z_rows,
                       double* residuals, CfSolveStats* stats);
+
+/* --- measurement ------------------------------------------------------- */
+/* the cudaStream_t every kernel of this hierarchy is launched on */
+void* cf_hier_stream(void* handle);
+/* enable (1) / disable (0) per-launch CUDA-event profiling; clears records.
+ * While enabled, V-cycles are launched eagerly instead of as a CUDA graph. */
+int cf_profile(void* handle, int32_t enable);
+/* aggregate of the recorded launches, one line per (kernel kind, level):
+ * "kind level launches total_ms algorithmic_bytes\n"; *needed = length. */
+int cf_profile_report(void* handle, char* buf, int64_t cap, int64_t* needed);
 
 /* --- host setup helpers (solver.py greedy loops) ---------------------- */
 /* solver.py:236-247: greedy ascending-id independent set of off-degree

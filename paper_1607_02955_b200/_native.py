@@ -78,11 +78,14 @@ _SIGS = {
     "cf_jl_rhs_rows": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
                                  C.c_int64, C.c_int64, C.c_int32, f64p]),
     "cf_jl_sketch": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
-                               C.c_int64, C.c_double, i64p, C.c_int64,
+                               C.c_int64, C.c_int64, C.c_int64, C.c_double, i64p, C.c_int64,
                                C.POINTER(CfSolveParams), f64p, f64p, f64p,
                                C.POINTER(CfSolveStats)]),
     "cf_node_solutions": (C.c_int, [C.c_void_p, i64p, C.c_int64, C.POINTER(CfSolveParams), f64p,
                                     f64p, f64p, C.POINTER(CfSolveStats)]),
+    "cf_hier_stream": (C.c_void_p, [C.c_void_p]),
+    "cf_profile": (C.c_int, [C.c_void_p, C.c_int32]),
+    "cf_profile_report": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int64, i64p]),
     "cf_setup_elim_select": (C.c_int, [C.c_int64, i64p, i64p, C.c_int32, i64p, i64p]),
     "cf_setup_aggregate": (C.c_int, [C.c_int64, i64p, i64p, f64p, C.c_int32, i64p, i64p]),
     "cf_setup_matching": (C.c_int, [C.c_int64, C.c_int64, i64p, i64p, i64p, i64p, i64p]),

@@ -11,6 +11,17 @@
 
 namespace cf {
 
+// Heavy-row plan of one CSR operator (see cf_kernels.cuh): heavy rows of each
+// colour class are numbered contiguously so one class's segments form a range.
+struct Plan {
+    int64_t nheavy = 0, nseg = 0;
+    int32_t* hv = nullptr;
+    int64_t* hsp = nullptr;
+    int64_t* sbeg = nullptr;
+    int64_t* send = nullptr;
+    std::vector<int64_t> cseg;  // class c -> segments [cseg[c], cseg[c+1])
+};
+
 struct DLevel {
     int kind = 0, n = 0, nc = 0, nf = 0, ncolors = 0;
     int64_t nnz = 0;
@@ -34,7 +45,27 @@ struct DLevel {
     double* b = nullptr;
     double* x = nullptr;
     double* ls = nullptr;  // 2 x 256 line-search sums
+    // per colour class (host, for the algorithmic-bytes model): rows, nnz,
+    // distinct neighbour rows
+    std::vector<int64_t> c_rows, c_nnz, c_nbr;
+    int64_t w_nnz = 0;  // elimination: nnz(W_cf)
+    int gs_classes = 0;  // colour classes swept one by one (<= kGsClasses)
+    bool merged = false; // classes >= kGsClasses merged into one Jacobi step
+    Plan pm;  // matrix rows (level 0 / aggregation levels)
+    Plan pw;  // W_cf rows (elimination levels)
 };
+
+// Per-launch profiling (CUDA events around every launch; cycles run eagerly).
+struct ProfRec {
+    const char* kind;
+    int level;
+    double bytes;
+    cudaEvent_t a, b;
+};
+
+// Multicolour GS sweeps the first kGsClasses colour classes one by one; the
+// remaining (small, hub-heavy) classes form one Jacobi step.
+constexpr int kGsClasses = 8;
 
 // Supported block widths (columns per device chunk).
 constexpr int kMaxKC = 256;
@@ -54,6 +85,10 @@ struct Hier {
     int kc_fb = 0;
     double* parts = nullptr;
     size_t parts_cap = 0;  // doubles
+    double* SP = nullptr;  // heavy-row segment partials, max_nseg x kc_ws
+    double* T = nullptr;   // merged-class Jacobi staging, max_merged x kc_ws
+    int64_t max_merged = 0;
+    int64_t max_nseg = 0;
     double* sums = nullptr;  // 8 x kMaxKC
     double* coef = nullptr;  // 4 x kMaxKC
     double *bn = nullptr, *res = nullptr, *prev = nullptr;
@@ -64,11 +99,28 @@ struct Hier {
     std::vector<void*> owned;   // operator allocations
     int64_t bytes = 0;
     std::map<int, cudaGraphExec_t> cycle_graphs;  // per KC
+    bool prof = false;
+    std::vector<ProfRec> recs;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    int prof_begin(const char* kind, int level, double bytes);
+    void prof_end(int idx);
 
     ~Hier();
     void* dalloc(size_t bytes_);
     void ensure_workspace(int kc);
     void ensure_fallback(int kc);
+};
+
+struct ProfScope {
+    Hier& h;
+    int idx = -1;
+    ProfScope(Hier& h_, const char* kind, int level, double bytes) : h(h_) {
+        if (h.prof) idx = h.prof_begin(kind, level, bytes);
+    }
+    ~ProfScope() {
+        if (idx >= 0) h.prof_end(idx);
+    }
 };
 
 // Solve a device block B (n0 x kc row-major, already in h.B) into h.X.

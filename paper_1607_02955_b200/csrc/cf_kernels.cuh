@@ -90,42 +90,98 @@ __device__ __forceinline__ void zero(DV<V>& r) {
     for (int t = 0; t < V; ++t) r.v[t] = 0.0;
 }
 
-// acc += sum_p val[p] * X[map(col[p]), c0 : c0+V]  over p in [beg, end), ascending p.
-template <int KC, bool MAPPED>
+// Gather modes: what the CSR entry (j, a) of a row multiplies.
+enum GatherMode { G_PLAIN = 0, G_MAPPED = 1, G_ELIM = 2 };
+
+// acc += sum_p val[p] * Y(col[p]) over p in [beg, end), ascending p (one fma
+// chain per column, identical for every block width), where
+//   G_PLAIN : Y(j) = X[j, :]
+//   G_MAPPED: Y(j) = X[map[j], :]                 (P xc gathers)
+//   G_ELIM  : Y(j) = X[map[j], :] / div[j]        (W_cf (b_f / d_f))
+// The working lanes of the warp load LPR consecutive (col, val) pairs with one
+// coalesced access and broadcast them by shuffle; up to 8 neighbour rows are
+// then in flight per warp.
+template <int KC, int MODE>
 __device__ __forceinline__ void gather_row(const int32_t* __restrict__ col,
                                            const double* __restrict__ val, int64_t beg,
                                            int64_t end, const int32_t* __restrict__ map,
+                                           const double* __restrict__ div,
                                            const double* __restrict__ X, int c0,
                                            DV<Lay<KC>::VEC>& acc) {
     constexpr int V = Lay<KC>::VEC;
-    int64_t p = beg;
-    for (; p + 4 <= end; p += 4) {
-        int j[4];
-        double a[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            j[u] = __ldg(col + p + u);
-            a[u] = __ldg(val + p + u);
+    constexpr int W = Lay<KC>::LPR;
+    constexpr unsigned MASK = W == 32 ? 0xffffffffu : ((1u << W) - 1u);
+    constexpr int G = W < 8 ? W : 8;
+    const int lane = threadIdx.x & 31;
+    for (int64_t p0 = beg; p0 < end; p0 += W) {
+        const int cnt = (int)min((int64_t)W, end - p0);
+        int jj = 0;
+        double aa = 0.0, dd = 1.0;
+        if (lane < cnt) {
+            jj = __ldg(col + p0 + lane);
+            aa = __ldg(val + p0 + lane);
+            if constexpr (MODE == G_ELIM) dd = __ldg(div + jj);
+            if constexpr (MODE != G_PLAIN) jj = __ldg(map + jj);
         }
-        if constexpr (MAPPED) {
+        for (int u0 = 0; u0 < cnt; u0 += G) {
+            DV<V> x[G];
+            double a[G], d[G];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) j[u] = __ldg(map + j[u]);
+            for (int u = 0; u < G; ++u) {
+                int j = __shfl_sync(MASK, jj, u0 + u, W);
+                a[u] = __shfl_sync(MASK, aa, u0 + u, W);
+                if constexpr (MODE == G_ELIM) d[u] = __shfl_sync(MASK, dd, u0 + u, W);
+                if (u0 + u < cnt)
+                    x[u] = ldv<V>(X + (size_t)j * KC + c0);
+                else
+                    zero(x[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < G; ++u) {
+                if (u0 + u < cnt) {
+#pragma unroll
+                    for (int t = 0; t < V; ++t) {
+                        if constexpr (MODE == G_ELIM)
+                            acc.v[t] = fma(a[u], x[u].v[t] / d[u], acc.v[t]);
+                        else
+                            acc.v[t] = fma(a[u], x[u].v[t], acc.v[t]);
+                    }
+                }
+            }
         }
-        DV<V> x[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) x[u] = ldv<V>(X + (size_t)j[u] * KC + c0);
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-            for (int t = 0; t < V; ++t) acc.v[t] = fma(a[u], x[u].v[t], acc.v[t]);
     }
-    for (; p < end; ++p) {
-        int j = __ldg(col + p);
-        double a = __ldg(val + p);
-        if constexpr (MAPPED) j = __ldg(map + j);
-        DV<V> x = ldv<V>(X + (size_t)j * KC + c0);
+}
+
+// Heavy rows (more than kHeavyNnz entries) are split into segments of at most
+// kSegNnz entries; k_seg computes each segment's partial sum into P[seg][KC]
+// and the row kernels add a heavy row's segment partials in segment order.
+constexpr int kHeavyNnz = 128;
+constexpr int kSegNnz = 128;
+
+struct HeavyDev {
+    const int32_t* hv = nullptr;   // row -> heavy index or -1
+    const int64_t* hsp = nullptr;  // heavy index -> first segment (size nheavy+1)
+    const double* P = nullptr;     // segment partials, [nseg][KC]
+};
+
+template <int KC, int MODE>
+__device__ __forceinline__ void row_sum(const HeavyDev& H, int64_t i,
+                                        const int32_t* __restrict__ col,
+                                        const double* __restrict__ val, int64_t beg, int64_t end,
+                                        const int32_t* __restrict__ map,
+                                        const double* __restrict__ div,
+                                        const double* __restrict__ X, int c0,
+                                        DV<Lay<KC>::VEC>& acc) {
+    constexpr int V = Lay<KC>::VEC;
+    const int hv = H.hv ? H.hv[i] : -1;
+    if (hv >= 0) {
+        for (int64_t sgi = H.hsp[hv]; sgi < H.hsp[hv + 1]; ++sgi) {
+            DV<V> q = ldv<V>(H.P + (size_t)sgi * KC + c0);
 #pragma unroll
-        for (int t = 0; t < V; ++t) acc.v[t] = fma(a, x.v[t], acc.v[t]);
+            for (int t = 0; t < V; ++t) acc.v[t] += q.v[t];
+        }
+    } else {
+        gather_row<KC, MODE>(col, val, beg, end, map, div, X, c0, acc);
     }
 }
 

@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(kThreads) k_residual(int n, const int64_t* __r
                                                        const double* __restrict__ X,
                                                        double* __restrict__ R,
                                                        double* __restrict__ parts,
-                                                       int64_t nparts) {
+                                                       int64_t nparts, HeavyDev H) {
     CF_LANE_SETUP(KC)
     extern __shared__ double smem[];
     DV<V> loc[2];
@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(kThreads) k_residual(int n, const int64_t* __r
         if (i >= n || !lane_ok) break;
         DV<V> acc;
         zero(acc);
-        gather_row<KC, false>(col, val, rp[i], rp[i + 1], nullptr, X, c0, acc);
+        row_sum<KC, G_PLAIN>(H, i, col, val, rp[i], rp[i + 1], nullptr, nullptr, X, c0, acc);
         DV<V> b = ldv<V>(B + i * KC + c0), x = ldv<V>(X + i * KC + c0);
         double d = diag[i];
         DV<V> out;
@@ -90,13 +90,13 @@ __global__ void __launch_bounds__(kThreads) k_spmm(int n, const int64_t* __restr
                                                    const double* __restrict__ val,
                                                    const double* __restrict__ diag,
                                                    const double* __restrict__ X,
-                                                   double* __restrict__ Y) {
+                                                   double* __restrict__ Y, HeavyDev H) {
     CF_LANE_SETUP(KC)
     int64_t i = (int64_t)blockIdx.x * Lt::RPB + slot;
     if (i >= n || !lane_ok) return;
     DV<V> acc;
     zero(acc);
-    gather_row<KC, false>(col, val, rp[i], rp[i + 1], nullptr, X, c0, acc);
+    row_sum<KC, G_PLAIN>(H, i, col, val, rp[i], rp[i + 1], nullptr, nullptr, X, c0, acc);
     DV<V> x = ldv<V>(X + i * KC + c0);
     double d = diag[i];
 #pragma unroll
@@ -307,19 +307,57 @@ __global__ void __launch_bounds__(kThreads) k_gs(const int32_t* __restrict__ row
                                                  const double* __restrict__ val,
                                                  const double* __restrict__ diag,
                                                  const double* __restrict__ B,
-                                                 double* __restrict__ X, int from_zero) {
+                                                 double* __restrict__ X, int from_zero,
+                                                 HeavyDev H) {
     CF_LANE_SETUP(KC)
     int64_t g = (int64_t)blockIdx.x * Lt::RPB + slot;
     if (g >= cnt || !lane_ok) return;
     int64_t i = rows[g];
     DV<V> acc;
     zero(acc);
-    if (!from_zero) gather_row<KC, false>(col, val, rp[i], rp[i + 1], nullptr, X, c0, acc);
+    if (!from_zero)
+        row_sum<KC, G_PLAIN>(H, i, col, val, rp[i], rp[i + 1], nullptr, nullptr, X, c0, acc);
     DV<V> b = ldv<V>(B + i * KC + c0);
     double d = diag[i];
 #pragma unroll
     for (int t = 0; t < V; ++t) acc.v[t] = (b.v[t] - acc.v[t]) / d;
     stv<V>(X + i * KC + c0, acc);
+}
+
+// Merged trailing colour classes, one Jacobi step: T[q] = (b_i - sum_j L_ij x_j) / L_ii
+// for i = rows[q] with every x_j read before any row of the step is written
+// (k_scatter_rows then writes T back).
+template <int KC>
+__global__ void __launch_bounds__(kThreads) k_jacobi_rows(const int32_t* __restrict__ rows, int cnt,
+                                                          const int64_t* __restrict__ rp,
+                                                          const int32_t* __restrict__ col,
+                                                          const double* __restrict__ val,
+                                                          const double* __restrict__ diag,
+                                                          const double* __restrict__ B,
+                                                          const double* __restrict__ X,
+                                                          double* __restrict__ T, HeavyDev H) {
+    CF_LANE_SETUP(KC)
+    int64_t g = (int64_t)blockIdx.x * Lt::RPB + slot;
+    if (g >= cnt || !lane_ok) return;
+    int64_t i = rows[g];
+    DV<V> acc;
+    zero(acc);
+    row_sum<KC, G_PLAIN>(H, i, col, val, rp[i], rp[i + 1], nullptr, nullptr, X, c0, acc);
+    DV<V> b = ldv<V>(B + i * KC + c0);
+    double d = diag[i];
+#pragma unroll
+    for (int t = 0; t < V; ++t) acc.v[t] = (b.v[t] - acc.v[t]) / d;
+    stv<V>(T + g * KC + c0, acc);
+}
+
+template <int KC>
+__global__ void __launch_bounds__(kThreads) k_scatter_rows(const int32_t* __restrict__ rows,
+                                                           int cnt, const double* __restrict__ T,
+                                                           double* __restrict__ X) {
+    CF_LANE_SETUP(KC)
+    int64_t g = (int64_t)blockIdx.x * Lt::RPB + slot;
+    if (g >= cnt || !lane_ok) return;
+    stv<V>(X + (size_t)rows[g] * KC + c0, ldv<V>(T + g * KC + c0));
 }
 
 // bc[a] = sum_{i in a} (b_i - L_i x)  (residual fused with P^T, solver.py:548-549)
@@ -328,7 +366,8 @@ __global__ void __launch_bounds__(kThreads) k_agg_restrict(
     int nc, const int32_t* __restrict__ aptr, const int32_t* __restrict__ amem,
     const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
     const double* __restrict__ val, const double* __restrict__ diag,
-    const double* __restrict__ B, const double* __restrict__ X, double* __restrict__ Bc) {
+    const double* __restrict__ B, const double* __restrict__ X, double* __restrict__ Bc,
+    HeavyDev H) {
     CF_LANE_SETUP(KC)
     int64_t a = (int64_t)blockIdx.x * Lt::RPB + slot;
     if (a >= nc || !lane_ok) return;
@@ -338,7 +377,7 @@ __global__ void __launch_bounds__(kThreads) k_agg_restrict(
         int64_t i = amem[q];
         DV<V> acc;
         zero(acc);
-        gather_row<KC, false>(col, val, rp[i], rp[i + 1], nullptr, X, c0, acc);
+        row_sum<KC, G_PLAIN>(H, i, col, val, rp[i], rp[i + 1], nullptr, nullptr, X, c0, acc);
         DV<V> b = ldv<V>(B + i * KC + c0), x = ldv<V>(X + i * KC + c0);
         double d = diag[i];
 #pragma unroll
@@ -355,7 +394,7 @@ __global__ void __launch_bounds__(kThreads) k_agg_ls(
     const double* __restrict__ val, const double* __restrict__ diag,
     const int32_t* __restrict__ agg, const double* __restrict__ Xc,
     const double* __restrict__ Bc, double* __restrict__ pden, int64_t pf,
-    double* __restrict__ pnum, int64_t pc) {
+    double* __restrict__ pnum, int64_t pc, HeavyDev H) {
     CF_LANE_SETUP(KC)
     extern __shared__ double smem[];
     DV<V> loc[1];
@@ -367,7 +406,7 @@ __global__ void __launch_bounds__(kThreads) k_agg_ls(
             if (i >= n || !lane_ok) break;
             DV<V> acc;
             zero(acc);
-            gather_row<KC, true>(col, val, rp[i], rp[i + 1], agg, Xc, c0, acc);
+            row_sum<KC, G_MAPPED>(H, i, col, val, rp[i], rp[i + 1], agg, nullptr, Xc, c0, acc);
             DV<V> d = ldv<V>(Xc + (size_t)agg[i] * KC + c0);
             double dg = diag[i];
 #pragma unroll
@@ -416,23 +455,37 @@ __global__ void __launch_bounds__(kThreads) k_elim_restrict(
     int nc, const int32_t* __restrict__ cn, const int64_t* __restrict__ wp,
     const int32_t* __restrict__ wc, const double* __restrict__ wv,
     const int32_t* __restrict__ fn, const double* __restrict__ fd,
-    const double* __restrict__ B, double* __restrict__ Bc) {
+    const double* __restrict__ B, double* __restrict__ Bc, HeavyDev H) {
     CF_LANE_SETUP(KC)
     int64_t i = (int64_t)blockIdx.x * Lt::RPB + slot;
     if (i >= nc || !lane_ok) return;
     DV<V> acc;
     zero(acc);
-    for (int64_t p = wp[i]; p < wp[i + 1]; ++p) {
-        int q = wc[p];
-        double w = wv[p], d = fd[q];
-        DV<V> b = ldv<V>(B + (size_t)fn[q] * KC + c0);
-#pragma unroll
-        for (int t = 0; t < V; ++t) acc.v[t] = fma(w, b.v[t] / d, acc.v[t]);
-    }
+    row_sum<KC, G_ELIM>(H, i, wc, wv, wp[i], wp[i + 1], fn, fd, B, c0, acc);
     DV<V> b = ldv<V>(B + (size_t)cn[i] * KC + c0);
 #pragma unroll
     for (int t = 0; t < V; ++t) acc.v[t] = b.v[t] + acc.v[t];
     stv<V>(Bc + i * KC + c0, acc);
+}
+
+// Partial sums of heavy-row segments: P[s] = sum over [sbeg[s], send[s]).
+template <int KC, int MODE>
+__global__ void __launch_bounds__(kThreads) k_seg(int64_t s_lo, int64_t s_hi,
+                                                  const int64_t* __restrict__ sbeg,
+                                                  const int64_t* __restrict__ send,
+                                                  const int32_t* __restrict__ col,
+                                                  const double* __restrict__ val,
+                                                  const int32_t* __restrict__ map,
+                                                  const double* __restrict__ div,
+                                                  const double* __restrict__ X,
+                                                  double* __restrict__ P) {
+    CF_LANE_SETUP(KC)
+    int64_t sg = s_lo + (int64_t)blockIdx.x * Lt::RPB + slot;
+    if (sg >= s_hi || !lane_ok) return;
+    DV<V> acc;
+    zero(acc);
+    gather_row<KC, MODE>(col, val, sbeg[sg], send[sg], map, div, X, c0, acc);
+    stv<V>(P + (size_t)sg * KC + c0, acc);
 }
 
 // x[c_i] = xc_i ; x[f] = (b_f + sum W_fc xc) / d_f   (solver.py:538-541)
@@ -454,7 +507,7 @@ __global__ void __launch_bounds__(kThreads) k_elim_interp(
     if (g >= nf) return;
     DV<V> acc;
     zero(acc);
-    gather_row<KC, false>(wc, wv, wp[g], wp[g + 1], nullptr, Xc, c0, acc);
+    gather_row<KC, G_PLAIN>(wc, wv, wp[g], wp[g + 1], nullptr, nullptr, Xc, c0, acc);
     int64_t i = fn[g];
     DV<V> b = ldv<V>(B + i * KC + c0);
     double d = fd[g];
@@ -463,24 +516,61 @@ __global__ void __launch_bounds__(kThreads) k_elim_interp(
     stv<V>(X + i * KC + c0, acc);
 }
 
-// coarsest: x = M b, M dense n x n (solver.py:406-419 restated as one operator)
+// coarsest: x = M b, M dense n x n (solver.py:406-419 restated as one operator).
+// Register-tiled fp64 GEMM: a CTA computes 32 rows x KC columns; every output
+// is one fma chain over l ascending (width-independent, deterministic).
+constexpr int kDenseTR = 32, kDenseTL = 16;
 template <int KC>
 __global__ void __launch_bounds__(kThreads) k_dense(int n, const double* __restrict__ M,
                                                     const double* __restrict__ B,
                                                     double* __restrict__ X) {
-    CF_LANE_SETUP(KC)
-    int64_t i = (int64_t)blockIdx.x * Lt::RPB + slot;
-    if (i >= n || !lane_ok) return;
-    DV<V> acc;
-    zero(acc);
-    const double* m = M + (size_t)i * n;
-    for (int l = 0; l < n; ++l) {
-        double a = __ldg(m + l);
-        DV<V> b = ldv<V>(B + (size_t)l * KC + c0);
+    constexpr int CG = KC >= 16 ? 16 : KC;             // column groups
+    constexpr int RG = kThreads / CG;                   // row groups
+    constexpr int RPT = (kDenseTR + RG - 1) / RG;       // rows per thread
+    constexpr int CPT = KC / CG;                        // columns per thread
+    __shared__ double sA[kDenseTL][kDenseTR + 1];
+    __shared__ double sB[kDenseTL][KC];
+    const int tid = threadIdx.x, tc = tid % CG, tr = tid / CG;
+    const int i0 = blockIdx.x * kDenseTR;
+    double acc[RPT][CPT];
 #pragma unroll
-        for (int t = 0; t < V; ++t) acc.v[t] = fma(a, b.v[t], acc.v[t]);
+    for (int r = 0; r < RPT; ++r)
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) acc[r][c] = 0.0;
+    for (int l0 = 0; l0 < n; l0 += kDenseTL) {
+        for (int e = tid; e < kDenseTR * kDenseTL; e += kThreads) {
+            int r = e / kDenseTL, t = e % kDenseTL;
+            sA[t][r] = (i0 + r < n && l0 + t < n) ? M[(size_t)(i0 + r) * n + l0 + t] : 0.0;
+        }
+        for (int e = tid; e < kDenseTL * KC; e += kThreads) {
+            int t = e / KC, c = e % KC;
+            sB[t][c] = (l0 + t < n) ? B[(size_t)(l0 + t) * KC + c] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int t = 0; t < kDenseTL; ++t) {
+            double a[RPT], bb[CPT];
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) {
+                int rr = tr + r * RG;
+                a[r] = rr < kDenseTR ? sA[t][rr] : 0.0;
+            }
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) bb[c] = sB[t][tc + c * CG];
+#pragma unroll
+            for (int r = 0; r < RPT; ++r)
+#pragma unroll
+                for (int c = 0; c < CPT; ++c) acc[r][c] = fma(a[r], bb[c], acc[r][c]);
+        }
+        __syncthreads();
     }
-    stv<V>(X + i * KC + c0, acc);
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+        int rr = tr + r * RG, i = i0 + rr;
+        if (rr < kDenseTR && i < n)
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) X[(size_t)i * KC + tc + c * CG] = acc[r][c];
+    }
 }
 
 // rows layout (cnt x n) -> block (n x KC), zero padding for columns >= cnt
@@ -535,21 +625,46 @@ static inline size_t red_smem() {
 template <int KC>
 static void finalize(Hier& h, const double* parts, int64_t nparts, int nq, int64_t qstride,
                      double* out) {
+    ProfScope ps(h, "finalize", -1, 8.0 * KC * nq * (nparts + 1));
     k_finalize<KC><<<nq, kThreads, 0, h.s>>>(parts, nparts, qstride, out);
 }
 
 template <int KC>
 struct Ops {
+    static double A(int64_t rows, int64_t nnz) { return 12.0 * nnz + 16.0 * rows; }
+    static double Vb(int64_t rows) { return 8.0 * KC * rows; }
+    static HeavyDev hd(const Hier& h, const Plan& pl) {
+        HeavyDev d;
+        if (pl.nheavy) {
+            d.hv = pl.hv;
+            d.hsp = pl.hsp;
+            d.P = h.SP;
+        }
+        return d;
+    }
+    // segment partials of a plan's segments [lo, hi)
+    template <int MODE>
+    static void seg(Hier& h, const Plan& pl, int64_t lo, int64_t hi, const int32_t* col,
+                    const double* val, const int32_t* map, const double* div, const double* X,
+                    int level) {
+        if (hi <= lo) return;
+        ProfScope ps(h, "heavy_seg", level, 12.0 * kSegNnz * (hi - lo) + Vb(hi - lo) * 2);
+        k_seg<KC, MODE><<<(unsigned)((hi - lo + Lay<KC>::RPB - 1) / Lay<KC>::RPB), kThreads, 0,
+                          h.s>>>(lo, hi, pl.sbeg, pl.send, col, val, map, div, X, h.SP);
+    }
     static void residual(Hier& h, const double* B, const double* X, double* R, double* sums2) {
         DLevel& l = h.L[0];
         int64_t np = nparts_of(l.n);
+        seg<G_PLAIN>(h, l.pm, 0, l.pm.nseg, l.col, l.val, nullptr, nullptr, X, 0);
+        ProfScope ps(h, "residual", 0, A(l.n, l.nnz) + Vb(l.n) * (R ? 3 : 2));
         k_residual<KC><<<(unsigned)np, kThreads, red_smem<KC, 2>(), h.s>>>(
-            l.n, l.rp, l.col, l.val, l.diag, B, X, R, h.parts, np);
+            l.n, l.rp, l.col, l.val, l.diag, B, X, R, h.parts, np, hd(h, l.pm));
         finalize<KC>(h, h.parts, np, 2, np * KC, sums2);
     }
     static void colsum(Hier& h, const double* X, const double* Y, double* out) {
         int n = h.n0;
         int64_t np = nparts_of(n);
+        ProfScope ps(h, "colsum", 0, Vb(n) * (Y ? 2 : 1));
         k_colsum<KC><<<(unsigned)np, kThreads, red_smem<KC, 1>(), h.s>>>(n, X, Y, h.parts, np);
         finalize<KC>(h, h.parts, np, 1, np * KC, out);
     }
@@ -557,19 +672,24 @@ struct Ops {
                      double* out) {
         int n = h.n0;
         int64_t np = nparts_of(n);
+        ProfScope ps(h, "fallback", 0, 0.0);
         k_dot2<KC><<<(unsigned)np, kThreads, red_smem<KC, 2>(), h.s>>>(n, a, b, c, d, h.parts,
                                                                       np);
         finalize<KC>(h, h.parts, np, 2, np * KC, out);
     }
     static void spmm(Hier& h, const double* X, double* Y) {
         DLevel& l = h.L[0];
+        seg<G_PLAIN>(h, l.pm, 0, l.pm.nseg, l.col, l.val, nullptr, nullptr, X, 0);
+        ProfScope ps(h, "fallback", 0, 0.0);
         k_spmm<KC><<<grid_rows<KC>(l.n), kThreads, 0, h.s>>>(l.n, l.rp, l.col, l.val, l.diag, X,
-                                                             Y);
+                                                             Y, hd(h, l.pm));
     }
     static void center(Hier& h, double* X, const double* mean) {
+        ProfScope ps(h, "center", 0, 2 * Vb(h.n0));
         k_center<KC><<<grid_rows<KC>(h.n0), kThreads, 0, h.s>>>(h.n0, X, mean);
     }
     static void lincomb(Hier& h, double* Y, const double* U, const double* W, const double* coef) {
+        ProfScope ps(h, "fallback", 0, 0.0);
         k_lincomb<KC><<<grid_rows<KC>(h.n0), kThreads, 0, h.s>>>(h.n0, Y, U, W, coef);
     }
 
@@ -583,9 +703,12 @@ struct Ops {
         double* x = bufx(h, j);
         if (l.kind == CF_LEVEL_COARSEST) {
             if (l.n == 1 || !l.M) {
+                ProfScope ps(h, "memset", j, Vb(l.n));
                 CF_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * (size_t)l.n * KC, h.s));
             } else {
-                k_dense<KC><<<grid_rows<KC>(l.n), kThreads, 0, h.s>>>(l.n, l.M, b, x);
+                ProfScope ps(h, "dense", j, 8.0 * l.n * l.n + 2 * Vb(l.n));
+                k_dense<KC><<<(unsigned)((l.n + kDenseTR - 1) / kDenseTR), kThreads, 0, h.s>>>(
+                    l.n, l.M, b, x);
             }
             return;
         }
@@ -593,39 +716,98 @@ struct Ops {
         double* bc = bufb(h, j + 1);
         double* xc = bufx(h, j + 1);
         if (l.kind == CF_LEVEL_ELIMINATION) {
-            k_elim_restrict<KC><<<grid_rows<KC>(l.nc), kThreads, 0, h.s>>>(
-                l.nc, l.cn, l.wcp, l.wcc, l.wcv, l.fn, l.fd, b, bc);
+            {
+                seg<G_ELIM>(h, l.pw, 0, l.pw.nseg, l.wcc, l.wcv, l.fn, l.fd, b, j);
+                ProfScope ps(h, "elim_restrict", j,
+                             12.0 * l.w_nnz + 12.0 * l.nc + 12.0 * l.nf + Vb(2 * l.nc + l.nf));
+                k_elim_restrict<KC><<<grid_rows<KC>(l.nc), kThreads, 0, h.s>>>(
+                    l.nc, l.cn, l.wcp, l.wcc, l.wcv, l.fn, l.fd, b, bc, hd(h, l.pw));
+            }
             cycle(h, j + 1, nu1, nu2);
+            ProfScope ps(h, "elim_interp", j,
+                         12.0 * l.w_nnz + 24.0 * l.nf + 4.0 * l.nc + Vb(2 * l.nc + 2 * l.nf));
             k_elim_interp<KC><<<grid_rows<KC>((int64_t)l.nc + l.nf), kThreads, 0, h.s>>>(
                 l.nf, l.nc, l.cn, l.fn, l.wfp, l.wfc, l.wfv, l.fd, b, xc, x);
             return;
         }
         // aggregation level
-        CF_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * (size_t)l.n * KC, h.s));
-        for (int s = 0; s < nu1; ++s)
-            for (int col = 0; col < l.ncolors; ++col) sweep(h, l, col, b, x, s == 0 && col == 0);
-        k_agg_restrict<KC><<<grid_rows<KC>(l.nc), kThreads, 0, h.s>>>(
-            l.nc, l.aptr, l.amem, l.rp, l.col, l.val, l.diag, b, x, bc);
+        {
+            ProfScope ps(h, "memset", j, Vb(l.n));
+            CF_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * (size_t)l.n * KC, h.s));
+        }
+        for (int s = 0; s < nu1; ++s) {
+            for (int col = 0; col < l.gs_classes; ++col) sweep(h, l, col, b, x, s == 0 && col == 0);
+            if (l.merged) jacobi(h, l, b, x);
+        }
+        {
+            seg<G_PLAIN>(h, l.pm, 0, l.pm.nseg, l.col, l.val, nullptr, nullptr, x, j);
+            ProfScope ps(h, "agg_restrict", j,
+                         A(l.n, l.nnz) + 4.0 * l.n + 4.0 * l.nc + Vb(2 * l.n + l.nc));
+            k_agg_restrict<KC><<<grid_rows<KC>(l.nc), kThreads, 0, h.s>>>(
+                l.nc, l.aptr, l.amem, l.rp, l.col, l.val, l.diag, b, x, bc, hd(h, l.pm));
+        }
         cycle(h, j + 1, nu1, nu2);
         int64_t pf = nparts_of(l.n), pc = nparts_of(l.nc);
-        k_agg_ls<KC><<<(unsigned)(pf + pc), kThreads, red_smem<KC, 1>(), h.s>>>(
-            l.n, l.nc, l.rp, l.col, l.val, l.diag, l.agg, xc, bc, h.parts, pf,
-            h.parts + pf * KC, pc);
+        {
+            seg<G_MAPPED>(h, l.pm, 0, l.pm.nseg, l.col, l.val, l.agg, nullptr, xc, j);
+            ProfScope ps(h, "agg_linesearch", j, A(l.n, l.nnz) + 4.0 * l.n + Vb(2 * l.nc));
+            k_agg_ls<KC><<<(unsigned)(pf + pc), kThreads, red_smem<KC, 1>(), h.s>>>(
+                l.n, l.nc, l.rp, l.col, l.val, l.diag, l.agg, xc, bc, h.parts, pf,
+                h.parts + pf * KC, pc, hd(h, l.pm));
+        }
         finalize<KC>(h, h.parts, pf, 1, 0, l.ls);
         finalize<KC>(h, h.parts + pf * KC, pc, 1, 0, l.ls + KC);
-        k_agg_correct<KC><<<grid_rows<KC>(l.n), kThreads, 0, h.s>>>(l.n, l.agg, x, xc, l.ls);
-        for (int s = 0; s < nu2; ++s)
-            for (int col = l.ncolors - 1; col >= 0; --col) sweep(h, l, col, b, x, false);
+        {
+            ProfScope ps(h, "agg_correct", j, 4.0 * l.n + Vb(2 * l.n + l.nc));
+            k_agg_correct<KC><<<grid_rows<KC>(l.n), kThreads, 0, h.s>>>(l.n, l.agg, x, xc, l.ls);
+        }
+        for (int s = 0; s < nu2; ++s) {
+            if (l.merged) jacobi(h, l, b, x);
+            for (int col = l.gs_classes - 1; col >= 0; --col) sweep(h, l, col, b, x, false);
+        }
         (void)c;
     }
     static void sweep(Hier& h, DLevel& l, int colr, const double* b, double* x, bool from_zero) {
         int beg = l.cptr[colr], cnt = l.cptr[colr + 1] - beg;
         if (cnt <= 0) return;
+        const int lev = (int)(&l - &h.L[0]);
+        if (!from_zero)
+            seg<G_PLAIN>(h, l.pm, l.pm.cseg[colr], l.pm.cseg[colr + 1], l.col, l.val, nullptr,
+                         nullptr, x, lev);
+        ProfScope ps(h, "gs_sweep", lev,
+                     12.0 * l.c_nnz[colr] + 20.0 * cnt +
+                         Vb(2 * cnt + (from_zero ? 0 : l.c_nbr[colr])));
         k_gs<KC><<<grid_rows<KC>(cnt), kThreads, 0, h.s>>>(l.crows + beg, cnt, l.rp, l.col, l.val,
-                                                         l.diag, b, x, from_zero ? 1 : 0);
+                                                         l.diag, b, x, from_zero ? 1 : 0,
+                                                         hd(h, l.pm));
+    }
+
+    static void jacobi(Hier& h, DLevel& l, const double* b, double* x) {
+        const int K = l.gs_classes;
+        int beg = l.cptr[K], cnt = l.cptr[l.ncolors] - beg;
+        if (cnt <= 0) return;
+        const int lev = (int)(&l - &h.L[0]);
+        seg<G_PLAIN>(h, l.pm, l.pm.cseg[K], l.pm.cseg[l.ncolors], l.col, l.val, nullptr, nullptr,
+                     x, lev);
+        int64_t nnz = 0, nbr = 0;
+        for (int c = K; c < l.ncolors; ++c) {
+            nnz += l.c_nnz[c];
+            nbr += l.c_nbr[c];
+        }
+        {
+            ProfScope ps(h, "jacobi_merged", lev, 12.0 * nnz + 20.0 * cnt + Vb(2 * cnt + nbr));
+            k_jacobi_rows<KC><<<grid_rows<KC>(cnt), kThreads, 0, h.s>>>(
+                l.crows + beg, cnt, l.rp, l.col, l.val, l.diag, b, x, h.T, hd(h, l.pm));
+        }
+        ProfScope ps(h, "jacobi_scatter", lev, Vb(2 * cnt) + 4.0 * cnt);
+        k_scatter_rows<KC><<<grid_rows<KC>(cnt), kThreads, 0, h.s>>>(l.crows + beg, cnt, h.T, x);
     }
 
     static void run_cycle(Hier& h, int nu1, int nu2) {
+        if (h.prof) {  // eager launches so every kernel can be bracketed by events
+            cycle(h, 0, nu1, nu2);
+            return;
+        }
         auto it = h.cycle_graphs.find(KC * 1000000 + nu1 * 1000 + nu2);
         if (it == h.cycle_graphs.end()) {
             cudaGraph_t g;
@@ -854,10 +1036,12 @@ __global__ void __launch_bounds__(kThreads) k_addc(int n, double* __restrict__ X
 
 template <int KC>
 void Ops<KC>::diag_scale(Hier& h, const double* Rd, double* Zd) {
+    ProfScope ps(h, "fallback", 0, 0.0);
     k_diag_scale<KC><<<grid_rows<KC>(h.n0), kThreads, 0, h.s>>>(h.n0, h.L[0].diag, Rd, Zd);
 }
 template <int KC>
 void Ops<KC>::k_add_const(Hier& h, double* Xd) {
+    ProfScope ps(h, "addc", 0, 16.0 * KC * h.n0);
     k_addc<KC><<<grid_rows<KC>(h.n0), kThreads, 0, h.s>>>(h.n0, Xd, h.coef);
 }
 
@@ -873,7 +1057,10 @@ static void solve_block_t(Hier& h, int ncols, const CfSolveParams& p, double* re
     // column statistics of B: balance check and norms (solver.py:672-679)
     {
         int64_t np = nparts_of(n);
-        k_colstats<KC><<<(unsigned)np, kThreads, red_smem<KC, 3>(), h.s>>>(n, h.B, h.parts, np);
+        {
+            ProfScope ps(h, "colstats", 0, 8.0 * KC * n);
+            k_colstats<KC><<<(unsigned)np, kThreads, red_smem<KC, 3>(), h.s>>>(n, h.B, h.parts, np);
+        }
         finalize<KC>(h, h.parts, np, 3, np * KC, h.sums);
         CF_CUDA(cudaMemcpyAsync(h.h_small, h.sums, sizeof(double) * 3 * KC,
                                 cudaMemcpyDeviceToHost, h.s));
@@ -918,10 +1105,12 @@ static void solve_block_t(Hier& h, int ncols, const CfSolveParams& p, double* re
         bool broke = false;
         for (int it = 0; it < p.max_cycles; ++it) {
             O::residual(h, h.B, h.X, h.R, h.sums);
-            k_status<KC><<<1, KC < 32 ? 32 : KC, 0, h.s>>>(n, h.sums, h.bn, h.res, h.prev, h.stall,
-                                                            h.state, mean, h.count, stop,
-                                                            p.stagnation_factor,
-                                                            p.stagnation_cycles, 0);
+            {
+                ProfScope ps(h, "status", 0, 0.0);
+                k_status<KC><<<1, KC < 32 ? 32 : KC, 0, h.s>>>(
+                    n, h.sums, h.bn, h.res, h.prev, h.stall, h.state, mean, h.count, stop,
+                    p.stagnation_factor, p.stagnation_cycles, 0);
+            }
             CF_CUDA(cudaMemcpyAsync(h.h_count, h.count, sizeof(int), cudaMemcpyDeviceToHost, h.s));
             CF_CUDA(cudaStreamSynchronize(h.s));
             int act = *h.h_count;
@@ -932,7 +1121,10 @@ static void solve_block_t(Hier& h, int ncols, const CfSolveParams& p, double* re
             O::center(h, h.R, mean);
             O::run_cycle(h, p.nu1, p.nu2);
             O::colsum(h, h.X, h.C, csum);
-            k_update<KC><<<grid_rows<KC>(n), kThreads, 0, h.s>>>(n, h.X, h.C, csum, h.state);
+            {
+                ProfScope ps(h, "update", 0, 3.0 * 8.0 * KC * n);
+                k_update<KC><<<grid_rows<KC>(n), kThreads, 0, h.s>>>(n, h.X, h.C, csum, h.state);
+            }
             st.vcycles += act;
             st.outer_iterations += 1;
         }
@@ -1049,10 +1241,12 @@ void solve_block(Hier& h, int kc, int ncols, const CfSolveParams& p, double* res
 
 void rows_to_block(Hier& h, const double* S_dev, int cnt, int kc, double* B_dev) {
     dim3 blk(32, 8), grd((h.n0 + 31) / 32, (kc + 31) / 32);
+    ProfScope ps(h, "transpose", 0, 16.0 * kc * h.n0);
     CF_DISPATCH(kc, (k_rows_to_block<K_><<<grd, blk, 0, h.s>>>(S_dev, cnt, h.n0, B_dev)));
 }
 void block_to_rows(Hier& h, const double* B_dev, int cnt, int kc, double* S_dev) {
     dim3 blk(32, 8), grd((h.n0 + 31) / 32, (kc + 31) / 32);
+    ProfScope ps(h, "transpose", 0, 16.0 * kc * h.n0);
     CF_DISPATCH(kc, (k_block_to_rows<K_><<<grd, blk, 0, h.s>>>(B_dev, cnt, h.n0, S_dev)));
 }
 void finalize_dev(Hier& h, const double* parts, int64_t nparts, int nq, int64_t qstride,
@@ -1079,6 +1273,7 @@ void* Hier::dalloc(size_t nb) {
 Hier::~Hier() {
     cudaSetDevice(dev);
     for (auto& kv : cycle_graphs) cudaGraphExecDestroy(kv.second);
+    for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     for (void* p : owned) cudaFree(p);
     for (auto& l : L) {
         cudaFree(l.b);
@@ -1092,6 +1287,8 @@ Hier::~Hier() {
     cudaFree(P);
     cudaFree(AP);
     cudaFree(parts);
+    cudaFree(SP);
+    cudaFree(T);
     cudaFree(S);
     if (h_count) cudaFreeHost(h_count);
     if (h_small) cudaFreeHost(h_small);
@@ -1124,6 +1321,8 @@ void Hier::ensure_workspace(int kc) {
     np = std::max<size_t>(np, 3 * (size_t)(nparts_of(n0) + 1));
     re(parts, np * kc);
     parts_cap = np * kc;
+    re(SP, (size_t)std::max<int64_t>(max_nseg, 1) * kc);
+    re(T, (size_t)std::max<int64_t>(max_merged, 1) * kc);
     if (Z) {
         cudaFree(Z); cudaFree(P); cudaFree(AP);
         Z = P = AP = nullptr;
@@ -1145,6 +1344,23 @@ void Hier::ensure_fallback(int kc) {
     kc_fb = kc_ws;
 }
 
+int Hier::prof_begin(const char* kind, int level, double bytes_) {
+    if (ev_used + 2 > ev_pool.size()) {
+        for (int t = 0; t < 64; ++t) {
+            cudaEvent_t e;
+            CF_CUDA(cudaEventCreate(&e));
+            ev_pool.push_back(e);
+        }
+    }
+    ProfRec r{kind, level, bytes_, ev_pool[ev_used], ev_pool[ev_used + 1]};
+    ev_used += 2;
+    CF_CUDA(cudaEventRecord(r.a, s));
+    recs.push_back(r);
+    return (int)recs.size() - 1;
+}
+
+void Hier::prof_end(int idx) { cudaEventRecord(recs[idx].b, s); }
+
 }  // namespace cf
 
 using namespace cf;
@@ -1159,6 +1375,44 @@ extern "C" int cf_device_count(void) {
     int c = 0;
     if (cudaGetDeviceCount(&c) != cudaSuccess) return 0;
     return c;
+}
+
+template <typename T>
+static T* upload(Hier& h, const T* src, size_t cnt);
+
+// Build the heavy-row plan of a CSR operator: rows visited in class order
+// (order == nullptr: natural order, one class).
+static Plan build_plan(Hier& h, int64_t n, const int64_t* rp, const int32_t* order,
+                       const int32_t* cls_ptr, int ncls) {
+    Plan pl;
+    std::vector<int32_t> hv(n, -1);
+    std::vector<int64_t> hsp{0}, sb, se;
+    if (!order) ncls = 1;
+    for (int c = 0; c < ncls; ++c) {
+        pl.cseg.push_back((int64_t)sb.size());
+        int64_t lo = order ? cls_ptr[c] : 0, hi = order ? cls_ptr[c + 1] : n;
+        for (int64_t q = lo; q < hi; ++q) {
+            int64_t i = order ? order[q] : q;
+            int64_t deg = rp[i + 1] - rp[i];
+            if (deg <= kHeavyNnz) continue;
+            hv[i] = (int32_t)pl.nheavy++;
+            for (int64_t b = rp[i]; b < rp[i + 1]; b += kSegNnz) {
+                sb.push_back(b);
+                se.push_back(std::min<int64_t>(b + kSegNnz, rp[i + 1]));
+            }
+            hsp.push_back((int64_t)sb.size());
+        }
+    }
+    pl.cseg.push_back((int64_t)sb.size());
+    pl.nseg = (int64_t)sb.size();
+    if (pl.nheavy) {
+        pl.hv = upload(h, hv.data(), hv.size());
+        pl.hsp = upload(h, hsp.data(), hsp.size());
+        pl.sbeg = upload(h, sb.data(), sb.size());
+        pl.send = upload(h, se.data(), se.size());
+    }
+    h.max_nseg = std::max(h.max_nseg, pl.nseg);
+    return pl;
 }
 
 template <typename T>
@@ -1195,17 +1449,45 @@ extern "C" int cf_hier_create(int32_t nlev, const CfLevelDesc* ds, int32_t devic
                 if (!l.col) l.col = (int32_t*)h->dalloc(8);
                 if (!l.val) l.val = (double*)h->dalloc(8);
                 l.diag = upload(*h, d.diag, (size_t)d.n);
+                if (d.kind == CF_LEVEL_AGGREGATION)
+                    l.pm = build_plan(*h, d.n, d.rowptr, d.color_rows, d.color_ptr, d.n_colors);
+                else
+                    l.pm = build_plan(*h, d.n, d.rowptr, nullptr, nullptr, 1);
             } else if (need_matrix) {
                 throw CfError(CF_DOMAIN, "level matrix missing");
             }
             if (d.kind == CF_LEVEL_AGGREGATION) {
                 l.ncolors = d.n_colors;
+                l.gs_classes = std::min(d.n_colors, kGsClasses);
+                l.merged = d.n_colors > kGsClasses;
+                if (l.merged)
+                    h->max_merged = std::max<int64_t>(
+                        h->max_merged, d.color_ptr[d.n_colors] - d.color_ptr[kGsClasses]);
                 l.cptr.assign(d.color_ptr, d.color_ptr + d.n_colors + 1);
                 l.crows = upload(*h, d.color_rows, (size_t)d.n);
                 l.agg = upload(*h, d.agg, (size_t)d.n);
                 l.aptr = upload(*h, d.agg_ptr, (size_t)d.n_coarse + 1);
                 l.amem = upload(*h, d.agg_members, (size_t)d.n);
                 l.ls = (double*)h->dalloc(sizeof(double) * 2 * kMaxKC);
+                // colour-class sizes for the algorithmic-bytes model
+                std::vector<int64_t> stamp(d.n, -1);
+                for (int c = 0; c < d.n_colors; ++c) {
+                    int64_t rows = d.color_ptr[c + 1] - d.color_ptr[c], nnz = 0, nbr = 0;
+                    for (int32_t q = d.color_ptr[c]; q < d.color_ptr[c + 1]; ++q) {
+                        int32_t i = d.color_rows[q];
+                        for (int64_t p = d.rowptr[i]; p < d.rowptr[i + 1]; ++p) {
+                            ++nnz;
+                            int32_t jn = d.col[p];
+                            if (stamp[jn] != c) {
+                                stamp[jn] = c;
+                                ++nbr;
+                            }
+                        }
+                    }
+                    l.c_rows.push_back(rows);
+                    l.c_nnz.push_back(nnz);
+                    l.c_nbr.push_back(nbr);
+                }
             } else if (d.kind == CF_LEVEL_ELIMINATION) {
                 l.nf = d.n_f;
                 l.fn = upload(*h, d.f_nodes, (size_t)d.n_f);
@@ -1215,6 +1497,8 @@ extern "C" int cf_hier_create(int32_t nlev, const CfLevelDesc* ds, int32_t devic
                 l.wcc = upload(*h, d.wcf_col, (size_t)d.wcf_ptr[d.n_coarse]);
                 l.wcv = upload(*h, d.wcf_val, (size_t)d.wcf_ptr[d.n_coarse]);
                 l.wfp = upload(*h, d.wfc_ptr, (size_t)d.n_f + 1);
+                l.w_nnz = d.wcf_ptr[d.n_coarse];
+                l.pw = build_plan(*h, d.n_coarse, d.wcf_ptr, nullptr, nullptr, 1);
                 l.wfc = upload(*h, d.wfc_col, (size_t)d.wfc_ptr[d.n_f]);
                 l.wfv = upload(*h, d.wfc_val, (size_t)d.wfc_ptr[d.n_f]);
                 if (!l.wcc) l.wcc = (int32_t*)h->dalloc(8);
@@ -1319,5 +1603,54 @@ extern "C" int cf_residual_dev(void* hp, const double* B_dev, const double* X_de
     CF_DISPATCH(kc, Ops<K_>::residual(h, B_dev, X_dev, R_dev, h.sums));
     CF_CUDA(cudaMemcpyAsync(colsq, h.sums + k, sizeof(double) * k, cudaMemcpyDeviceToHost, h.s));
     CF_CUDA(cudaStreamSynchronize(h.s));
+    CF_API_END
+}
+
+extern "C" void* cf_hier_stream(void* hp) { return (void*)((Hier*)hp)->s; }
+
+extern "C" int cf_profile(void* hp, int32_t enable) {
+    CF_API_BEGIN
+    Hier& h = *(Hier*)hp;
+    std::lock_guard<std::mutex> lk(h.mu);
+    CF_CUDA(cudaStreamSynchronize(h.s));
+    h.prof = enable != 0;
+    h.recs.clear();
+    h.ev_used = 0;
+    CF_API_END
+}
+
+// One line per (kind, level): "kind level launches total_ms total_bytes\n".
+// Returns the number of bytes needed (excluding NUL) through *needed.
+extern "C" int cf_profile_report(void* hp, char* buf, int64_t cap, int64_t* needed) {
+    CF_API_BEGIN
+    Hier& h = *(Hier*)hp;
+    std::lock_guard<std::mutex> lk(h.mu);
+    CF_CUDA(cudaStreamSynchronize(h.s));
+    struct Agg {
+        int64_t launches = 0;
+        double ms = 0, bytes = 0;
+    };
+    std::map<std::pair<std::string, int>, Agg> agg;
+    for (auto& r : h.recs) {
+        float ms = 0.f;
+        CF_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+        Agg& a = agg[{r.kind, r.level}];
+        a.launches += 1;
+        a.ms += ms;
+        a.bytes += r.bytes;
+    }
+    std::string out;
+    char line[256];
+    for (auto& kv : agg) {
+        snprintf(line, sizeof line, "%s %d %lld %.6f %.1f\n", kv.first.first.c_str(),
+                 kv.first.second, (long long)kv.second.launches, kv.second.ms, kv.second.bytes);
+        out += line;
+    }
+    *needed = (int64_t)out.size();
+    if (buf && cap > 0) {
+        size_t nb = std::min<size_t>(out.size(), (size_t)cap - 1);
+        std::memcpy(buf, out.data(), nb);
+        buf[nb] = 0;
+    }
     CF_API_END
 }

@@ -200,21 +200,25 @@ def _pcg_words(seed: int):
 
 
 def _sketch_device(g: Graph, hierarchy: MultigridHierarchy, epsilon: float, seed: int,
-                   config: SolverConfig, query: np.ndarray | None, want_z: bool):
+                   config: SolverConfig, query: np.ndarray | None, want_z: bool,
+                   rows: tuple[int, int] | None = None):
+    """Device JL sketch of rows [r0, r1) (all k rows by default).  Returns
+    (k, z rows|None, additive per-query sums over those rows, residuals)."""
     if not 0 < epsilon <= 1:
         raise DomainError(f"epsilon must be in (0, 1], got {epsilon}")
     n = g.n
     if hierarchy.n != n:
         raise DomainError("hierarchy does not match graph")
     k = sketch_dimension(n, epsilon)
+    r0, r1 = (0, k) if rows is None else rows
     dg = _device_graph(g, hierarchy)
     q = np.zeros(0, dtype=np.int64) if query is None else np.ascontiguousarray(query, np.int64)
     sums = np.zeros(max(q.size, 1))
-    z = np.empty((k, n)) if want_z else None
-    res = np.zeros(k)
+    z = np.empty((r1 - r0, n)) if want_z else None
+    res = np.zeros(r1 - r0)
     st = N.CfSolveStats()
     sh, sl, ih, il = _pcg_words(seed)
-    N.check(N.lib().cf_jl_sketch(dg.handle, sh, sl, ih, il, k, 1.0 / math.sqrt(k),
+    N.check(N.lib().cf_jl_sketch(dg.handle, sh, sl, ih, il, k, r0, r1 - r0, 1.0 / math.sqrt(k),
                                  N.ptr(q, N.i64p), q.size, N.C.byref(_params(config, n)),
                                  N.ptr(sums, N.f64p), N.ptr(z, N.f64p), N.ptr(res, N.f64p),
                                  N.C.byref(st)), st)
@@ -247,11 +251,14 @@ def jl_rhs_rows(g: Graph, hierarchy: MultigridHierarchy, k: int, seed: int, row0
 
 
 def sketch_closeness_sums(g: Graph, hierarchy: MultigridHierarchy, epsilon: float, seed: int,
-                          query: Sequence[int], config: SolverConfig | None = None):
-    """Fused device JL path: returns (k, sums_v for query, residuals)."""
+                          query: Sequence[int], config: SolverConfig | None = None,
+                          rows: tuple[int, int] | None = None):
+    """Fused device JL path: returns (k, sums_v for query, residuals).  With
+    ``rows`` only that range of sketch rows is solved and the sums are its
+    additive share (multi-GPU sharding)."""
     config = config or hierarchy.config
     k, _, sums, res = _sketch_device(g, hierarchy, epsilon, seed, config,
-                                     np.asarray(query, dtype=np.int64), False)
+                                     np.asarray(query, dtype=np.int64), False, rows)
     return k, sums, res
 
 

@@ -54,6 +54,13 @@ STAGNATION_CYCLES = 5
 FCG_MAX_ITERS = 200
 BLOCK_COLUMNS = 64     # reference block width; the device solves all columns of a call at once
 STOP_MARGIN = 0.9
+# Device hierarchy truncation (B200 design choice): the device copy
+# of the hierarchy ends at the first level below the top with at most
+# min(DEVICE_DIRECT_MAX, n0 * DEVICE_DIRECT_FRACTION) nodes; that level is
+# solved exactly with its dense centred grounded inverse (one fp64 GEMM per
+# V-cycle) instead of recursing through the deep tail of tiny levels.
+DEVICE_DIRECT_MAX = 4096
+DEVICE_DIRECT_FRACTION = 1.0 / 16.0
 
 
 @dataclass(frozen=True)
@@ -129,15 +136,49 @@ class SolveStats:
             self.vcycles += vcycles
 
 
+_DEVICE: int | None = None
+
+
+def set_device(index: int) -> None:
+    """Select the CUDA device new hierarchies are uploaded to (one process
+    per GPU; defaults to $LOCAL_RANK or 0)."""
+    global _DEVICE
+    _DEVICE = int(index)
+
+
+def _device_index() -> int:
+    if _DEVICE is not None:
+        return _DEVICE
+    import os
+    return int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def device_levels(levels: list[Level]) -> list[Level]:
+    """The level list uploaded to the device: the host hierarchy truncated at
+    the first level j >= 1 with n_j <= min(DEVICE_DIRECT_MAX, n0/16), which
+    becomes the (exactly solved) coarsest level."""
+    n0 = levels[0].size
+    cap = min(DEVICE_DIRECT_MAX, int(n0 * DEVICE_DIRECT_FRACTION))
+    for j in range(1, len(levels) - 1):
+        if levels[j].size <= cap:
+            last = Level(kind=LevelKind.COARSEST, matrix=levels[j].matrix,
+                         grounded_factor=_factor_coarsest(levels[j].matrix))
+            return list(levels[:j]) + [last]
+    return list(levels)
+
+
 class _DeviceHierarchy:
     """Owner of the C handle (device operators + workspace)."""
 
-    def __init__(self, levels: list[Level], device: int = 0):
+    def __init__(self, levels: list[Level], device: int | None = None):
+        device = _device_index() if device is None else device
         L = N.lib()
         if L.cf_device_count() < 1:
             raise RuntimeError("cfcent_b200: no CUDA device visible; the solve path has no "
                                "CPU fallback")
         self._keep = []
+        levels = device_levels(levels)
+        self.levels = levels
         descs = (N.CfLevelDesc * len(levels))()
         for j, lvl in enumerate(levels):
             self._fill(descs[j], lvl, j)
@@ -246,6 +287,28 @@ class MultigridHierarchy:
 
     def device_bytes(self) -> int:
         return int(N.lib().cf_hier_device_bytes(self.device().handle))
+
+    def stream_ptr(self) -> int:
+        """cudaStream_t (as int) all kernels of this hierarchy run on."""
+        return int(N.lib().cf_hier_stream(self.device().handle) or 0)
+
+    def profile(self, enable: bool) -> None:
+        N.check(N.lib().cf_profile(self.device().handle, 1 if enable else 0))
+
+    def profile_report(self) -> list[tuple[str, int, int, float, float]]:
+        """[(kind, level, launches, total_ms, algorithmic_bytes)] of the launches
+        recorded since ``profile(True)``."""
+        need = np.zeros(1, dtype=np.int64)
+        L = N.lib()
+        N.check(L.cf_profile_report(self.device().handle, None, 0, N.ptr(need, N.i64p)))
+        buf = N.C.create_string_buffer(int(need[0]) + 1)
+        N.check(L.cf_profile_report(self.device().handle, buf, int(need[0]) + 1,
+                                    N.ptr(need, N.i64p)))
+        out = []
+        for line in buf.value.decode().splitlines():
+            k, lv, la, ms, by = line.split()
+            out.append((k, int(lv), int(la), float(ms), float(by)))
+        return out
 
 
 @dataclass

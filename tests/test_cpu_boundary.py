@@ -18,7 +18,7 @@ from paper_1607_02955_b200.solver import LevelKind, coarsen_aggregate, coarsen_e
 
 def header_symbols():
     txt = open(os.path.join(ROOT, "include", "cfcent_b200.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(cf_\w+)\s*\(", txt, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*|void\*)\s+(cf_\w+)\s*\(", txt, re.M)))
 
 
 def test_library_exports_header_symbols():
