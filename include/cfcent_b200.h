@@ -101,6 +101,11 @@ int cf_version(void);
 int cf_hier_create(int32_t n_levels, const CfLevelDesc* levels, int32_t device,
                    void** out_handle);
 int cf_hier_destroy(void* handle);
+/* Device node order: device row i of level 0 holds node perm[i] (a locality
+ * ordering chosen at upload; level descriptors are given in that order).
+ * All node-indexed host/device buffers of the API stay in node order; the
+ * library permutes at the boundary.  Not calling it means identity. */
+int cf_hier_set_order(void* handle, const int32_t* perm, int64_t n);
 /* total device bytes owned by the hierarchy (operators + workspace) */
 int64_t cf_hier_device_bytes(void* handle);
 

@@ -66,6 +66,7 @@ _SIGS = {
                                  C.POINTER(C.c_void_p)]),
     "cf_hier_destroy": (C.c_int, [C.c_void_p]),
     "cf_hier_device_bytes": (C.c_int64, [C.c_void_p]),
+    "cf_hier_set_order": (C.c_int, [C.c_void_p, i32p, C.c_int64]),
     "cf_solve_rows": (C.c_int, [C.c_void_p, f64p, C.c_int64, C.POINTER(CfSolveParams), f64p,
                                 f64p, C.POINTER(CfSolveStats)]),
     "cf_solve_block_dev": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,

@@ -20,6 +20,10 @@ struct Plan {
     int64_t* sbeg = nullptr;
     int64_t* send = nullptr;
     std::vector<int64_t> cseg;  // class c -> segments [cseg[c], cseg[c+1])
+    int32_t* seg_hv = nullptr;  // segment -> heavy index
+    int32_t* h_row = nullptr;   // heavy index -> row
+    int32_t* h_pos = nullptr;   // heavy index -> position in class order
+    int* cntr = nullptr;        // arrival counters (zero between launches)
 };
 
 struct DLevel {
@@ -31,6 +35,7 @@ struct DLevel {
     double* diag = nullptr;
     std::vector<int32_t> cptr;  // host copy of colour offsets
     int32_t* crows = nullptr;
+    bool contig = false;  // colour classes are contiguous row ranges (crows == identity)
     int32_t *agg = nullptr, *aptr = nullptr, *amem = nullptr;
     int32_t *fn = nullptr, *cn = nullptr;
     double* fd = nullptr;
@@ -65,7 +70,7 @@ struct ProfRec {
 
 // Multicolour GS sweeps the first kGsClasses colour classes one by one; the
 // remaining (small, hub-heavy) classes form one Jacobi step.
-constexpr int kGsClasses = 8;
+constexpr int kGsClasses = 2;
 
 // Supported block widths (columns per device chunk).
 constexpr int kMaxKC = 256;
@@ -78,6 +83,7 @@ struct Hier {
     std::mutex mu;
     int kc_ws = 0;  // workspace width currently allocated
     int n0 = 0;
+    int32_t* perm0 = nullptr;  // device row i holds node perm0[i] (nullptr: identity)
     // level-0 block buffers, n0 x kc_ws
     double *B = nullptr, *X = nullptr, *R = nullptr, *C = nullptr;
     // fallback buffers (lazily allocated)
@@ -86,6 +92,7 @@ struct Hier {
     double* parts = nullptr;
     size_t parts_cap = 0;  // doubles
     double* SP = nullptr;  // heavy-row segment partials, max_nseg x kc_ws
+    double* fin = nullptr; // finalize stage-1 scratch
     double* T = nullptr;   // merged-class Jacobi staging, max_merged x kc_ws
     int64_t max_merged = 0;
     int64_t max_nseg = 0;

@@ -18,7 +18,11 @@ namespace cf {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kRowsPerPart = 256;
+constexpr int kRowsPerPart = 64;
+#ifndef CF_GATHER_CTAS
+#define CF_GATHER_CTAS 3
+#endif
+constexpr int kGatherCtas = CF_GATHER_CTAS;  // min CTAs per SM for sweep kernels (register cap)
 
 // One row group per warp for every width: the row -> (warp, pass) mapping and
 // hence every reduction order is identical for all KC, so a column's result
@@ -111,18 +115,31 @@ __device__ __forceinline__ void gather_row(const int32_t* __restrict__ col,
     constexpr int V = Lay<KC>::VEC;
     constexpr int W = Lay<KC>::LPR;
     constexpr unsigned MASK = W == 32 ? 0xffffffffu : ((1u << W) - 1u);
-    constexpr int G = W < 8 ? W : 8;
+    // rows in flight per group: 24 doubles of row data (48 registers), so the
+    // gather kernels fit 3 CTAs of 256 threads per SM
+#ifndef CF_GATHER_DOUBLES
+#define CF_GATHER_DOUBLES 16
+#endif
+    constexpr int G0 = CF_GATHER_DOUBLES / V;
+    constexpr int G = W < G0 ? W : G0;
     const int lane = threadIdx.x & 31;
-    for (int64_t p0 = beg; p0 < end; p0 += W) {
-        const int cnt = (int)min((int64_t)W, end - p0);
-        int jj = 0;
-        double aa = 0.0, dd = 1.0;
-        if (lane < cnt) {
+    auto fetch = [&](int64_t p0, int& jj, double& aa, double& dd) {
+        jj = 0;
+        aa = 0.0;
+        dd = 1.0;
+        if (p0 + lane < end && lane < W) {
             jj = __ldg(col + p0 + lane);
             aa = __ldg(val + p0 + lane);
             if constexpr (MODE == G_ELIM) dd = __ldg(div + jj);
             if constexpr (MODE != G_PLAIN) jj = __ldg(map + jj);
         }
+    };
+    int jj, jn;
+    double aa, dd, an, dn;
+    fetch(beg, jj, aa, dd);
+    for (int64_t p0 = beg; p0 < end; p0 += W) {
+        const int cnt = (int)min((int64_t)W, end - p0);
+        fetch(p0 + W, jn, an, dn);  // next chunk's indices overlap this chunk's row loads
         for (int u0 = 0; u0 < cnt; u0 += G) {
             DV<V> x[G];
             double a[G], d[G];
@@ -149,20 +166,73 @@ __device__ __forceinline__ void gather_row(const int32_t* __restrict__ col,
                 }
             }
         }
+        jj = jn;
+        aa = an;
+        dd = dn;
     }
 }
 
 // Heavy rows (more than kHeavyNnz entries) are split into segments of at most
 // kSegNnz entries; k_seg computes each segment's partial sum into P[seg][KC]
 // and the row kernels add a heavy row's segment partials in segment order.
-constexpr int kHeavyNnz = 128;
-constexpr int kSegNnz = 128;
+constexpr int kHeavyNnz = 64;
+constexpr int kSegNnz = 64;
 
 struct HeavyDev {
     const int32_t* hv = nullptr;   // row -> heavy index or -1
     const int64_t* hsp = nullptr;  // heavy index -> first segment (size nheavy+1)
     const double* P = nullptr;     // segment partials, [nseg][KC]
 };
+
+// In-kernel heavy rows for the smoother sweeps: the launch carries extra warps,
+// one per segment [s_lo, s_hi); each writes its partial to SP, and the warp that
+// completes a heavy row (per-row arrival counter) sums the row's partials in
+// segment order and finalises the row.  The sum order is fixed; only which warp
+// performs it varies.
+struct SegWork {
+    int64_t s_lo = 0, s_hi = 0;
+    const int64_t* sbeg = nullptr;
+    const int64_t* send = nullptr;
+    const int32_t* seg_hv = nullptr;  // segment -> heavy index
+    const int64_t* hsp = nullptr;
+    const int32_t* h_row = nullptr;   // heavy index -> row
+    const int32_t* h_pos = nullptr;   // heavy index -> position in the class-ordered row list
+    int* cntr = nullptr;              // heavy index -> arrivals (kept zero between launches)
+    double* SP = nullptr;
+};
+
+template <int KC>
+__device__ __forceinline__ bool seg_item(const SegWork& w, int64_t s,
+                                         const int32_t* __restrict__ col,
+                                         const double* __restrict__ val,
+                                         const double* __restrict__ X, int c0, int& hv_out,
+                                         DV<Lay<KC>::VEC>& acc) {
+    constexpr int V = Lay<KC>::VEC;
+    constexpr int W = Lay<KC>::LPR;
+    constexpr unsigned MASK = W == 32 ? 0xffffffffu : ((1u << W) - 1u);
+    const int lane = threadIdx.x & 31;
+    zero(acc);
+    gather_row<KC, G_PLAIN>(col, val, w.sbeg[s], w.send[s], nullptr, nullptr, X, c0, acc);
+    stv<V>(w.SP + (size_t)s * KC + c0, acc);
+    __threadfence();
+    __syncwarp(MASK);
+    const int hv = w.seg_hv[s];
+    const int nsg = (int)(w.hsp[hv + 1] - w.hsp[hv]);
+    int old = 0;
+    if (lane == 0) old = atomicAdd(w.cntr + hv, 1);
+    old = __shfl_sync(MASK, old, 0);
+    if (old != nsg - 1) return false;
+    __threadfence();
+    zero(acc);
+    for (int64_t sg = w.hsp[hv]; sg < w.hsp[hv + 1]; ++sg) {
+        const double* q = w.SP + (size_t)sg * KC + c0;
+#pragma unroll
+        for (int t = 0; t < V; ++t) acc.v[t] += __ldcg(q + t);
+    }
+    if (lane == 0) w.cntr[hv] = 0;
+    hv_out = hv;
+    return true;
+}
 
 template <int KC, int MODE>
 __device__ __forceinline__ void row_sum(const HeavyDev& H, int64_t i,
@@ -173,7 +243,9 @@ __device__ __forceinline__ void row_sum(const HeavyDev& H, int64_t i,
                                         const double* __restrict__ X, int c0,
                                         DV<Lay<KC>::VEC>& acc) {
     constexpr int V = Lay<KC>::VEC;
-    const int hv = H.hv ? H.hv[i] : -1;
+    // heavy <=> more than kHeavyNnz entries (how the plan was built), so the
+    // row-to-heavy-index lookup is only paid by heavy rows
+    const int hv = (H.hv && end - beg > kHeavyNnz) ? H.hv[i] : -1;
     if (hv >= 0) {
         for (int64_t sgi = H.hsp[hv]; sgi < H.hsp[hv + 1]; ++sgi) {
             DV<V> q = ldv<V>(H.P + (size_t)sgi * KC + c0);

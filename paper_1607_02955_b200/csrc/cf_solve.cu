@@ -47,7 +47,7 @@ enum ColState { COL_ZERO = 0, COL_ACTIVE = 1, COL_CONV = 2, COL_FALLBACK = 3 };
 
 // R = B - L X ; partials of sum(R), sum(R^2)  (solver.py:694-695)
 template <int KC>
-__global__ void __launch_bounds__(kThreads) k_residual(int n, const int64_t* __restrict__ rp,
+__global__ void __launch_bounds__(kThreads, 2) k_residual(int n, const int64_t* __restrict__ rp,
                                                        const int32_t* __restrict__ col,
                                                        const double* __restrict__ val,
                                                        const double* __restrict__ diag,
@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(kThreads) k_residual(int n, const int64_t* __r
 
 // Y = L X (full Laplacian product) -- fallback Krylov solvers (solver.py:571-648)
 template <int KC>
-__global__ void __launch_bounds__(kThreads) k_spmm(int n, const int64_t* __restrict__ rp,
+__global__ void __launch_bounds__(kThreads, 2) k_spmm(int n, const int64_t* __restrict__ rp,
                                                    const int32_t* __restrict__ col,
                                                    const double* __restrict__ val,
                                                    const double* __restrict__ diag,
@@ -186,26 +186,32 @@ __global__ void __launch_bounds__(kThreads) k_colsum(int n, const double* __rest
 // out[q*KC + c] = sum_p parts[q*qstride + p*KC + c] in a canonical order that
 // depends on nparts only: 8 contiguous segments summed left to right, then the
 // segment sums in order.
-constexpr int kFinSeg = 8;
+// Canonical two-level order (depends on nparts only): segments of kFinSeg
+// consecutive parts summed left to right, then the segment sums in order.
+constexpr int kFinSeg = 64;
+// stage 1: grid (nseg, nq); out1[q][seg][KC]
 template <int KC>
-__global__ void __launch_bounds__(kThreads) k_finalize(const double* __restrict__ parts,
-                                                       int64_t nparts, int64_t qstride,
-                                                       double* __restrict__ out) {
-    __shared__ double sm[kFinSeg * KC];
-    const int q = blockIdx.x;
+__global__ void __launch_bounds__(kThreads) k_fin1(const double* __restrict__ parts,
+                                                   int64_t nparts, int64_t qstride,
+                                                   double* __restrict__ out1, int64_t nseg) {
+    const int q = blockIdx.y;
+    const int64_t seg = blockIdx.x;
     const double* p0 = parts + (size_t)q * qstride;
-    const int64_t per = (nparts + kFinSeg - 1) / kFinSeg;
-    for (int task = threadIdx.x; task < kFinSeg * KC; task += blockDim.x) {
-        const int c = task % KC, seg = task / KC;
-        const int64_t beg = seg * per, end = min(nparts, beg + per);
+    const int64_t beg = seg * kFinSeg, end = min(nparts, beg + kFinSeg);
+    for (int c = threadIdx.x; c < KC; c += blockDim.x) {
         double s = 0.0;
         for (int64_t p = beg; p < end; ++p) s += p0[p * KC + c];
-        sm[task] = s;
+        out1[((size_t)q * nseg + seg) * KC + c] = s;
     }
-    __syncthreads();
+}
+// stage 2 (or the only stage when nparts <= kFinSeg): grid nq
+template <int KC>
+__global__ void __launch_bounds__(kThreads) k_fin2(const double* __restrict__ in, int64_t cnt,
+                                                   int64_t qstride, double* __restrict__ out) {
+    const int q = blockIdx.x;
     for (int c = threadIdx.x; c < KC; c += blockDim.x) {
         double t = 0.0;
-        for (int g = 0; g < kFinSeg; ++g) t += sm[g * KC + c];
+        for (int64_t g = 0; g < cnt; ++g) t += in[(size_t)q * qstride + g * KC + c];
         out[q * KC + c] = t;
     }
 }
@@ -300,23 +306,45 @@ __global__ void __launch_bounds__(kThreads) k_lincomb(int n, double* __restrict_
 // x_i = (b_i - sum_{j != i} L_ij x_j) / L_ii.  Rows of one colour are pairwise
 // non-adjacent, so the class updates in parallel with exactly the values a
 // sequential sweep in colour order would use.  from_zero: x_i = b_i / L_ii.
+// Warps [0, cnt) take the class's rows (light rows only unless from_zero);
+// warps [cnt, cnt + nseg) take heavy-row segments (SegWork).
 template <int KC>
-__global__ void __launch_bounds__(kThreads) k_gs(const int32_t* __restrict__ rows, int cnt,
-                                                 const int64_t* __restrict__ rp,
-                                                 const int32_t* __restrict__ col,
-                                                 const double* __restrict__ val,
-                                                 const double* __restrict__ diag,
-                                                 const double* __restrict__ B,
-                                                 double* __restrict__ X, int from_zero,
-                                                 HeavyDev H) {
+__global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : kGatherCtas)) k_gs(const int32_t* __restrict__ rows,
+                                                              int base, int cnt,
+                                                              const int64_t* __restrict__ rp,
+                                                              const int32_t* __restrict__ col,
+                                                              const double* __restrict__ val,
+                                                              const double* __restrict__ diag,
+                                                              const double* __restrict__ B,
+                                                              double* __restrict__ X,
+                                                              int from_zero, HeavyDev H,
+                                                              SegWork w) {
     CF_LANE_SETUP(KC)
     int64_t g = (int64_t)blockIdx.x * Lt::RPB + slot;
-    if (g >= cnt || !lane_ok) return;
-    int64_t i = rows[g];
+    if (!lane_ok) return;
+    int64_t i;
     DV<V> acc;
     zero(acc);
-    if (!from_zero)
-        row_sum<KC, G_PLAIN>(H, i, col, val, rp[i], rp[i + 1], nullptr, nullptr, X, c0, acc);
+    if (g < cnt) {
+        i = rows ? (int64_t)rows[g] : base + g;
+        if (!from_zero) {
+            const int64_t beg = rp[i], end = rp[i + 1];
+            if (H.hv && end - beg > kHeavyNnz) return;  // finished by its last segment warp
+            DV<V> b = ldv<V>(B + i * KC + c0);
+            const double d = diag[i];
+            gather_row<KC, G_PLAIN>(col, val, beg, end, nullptr, nullptr, X, c0, acc);
+#pragma unroll
+            for (int t = 0; t < V; ++t) acc.v[t] = (b.v[t] - acc.v[t]) / d;
+            stv<V>(X + i * KC + c0, acc);
+            return;
+        }
+    } else {
+        int64_t s = w.s_lo + (g - cnt);
+        if (s >= w.s_hi) return;
+        int hv;
+        if (!seg_item<KC>(w, s, col, val, X, c0, hv, acc)) return;
+        i = w.h_row[hv];
+    }
     DV<V> b = ldv<V>(B + i * KC + c0);
     double d = diag[i];
 #pragma unroll
@@ -326,43 +354,60 @@ __global__ void __launch_bounds__(kThreads) k_gs(const int32_t* __restrict__ row
 
 // Merged trailing colour classes, one Jacobi step: T[q] = (b_i - sum_j L_ij x_j) / L_ii
 // for i = rows[q] with every x_j read before any row of the step is written
-// (k_scatter_rows then writes T back).
+// (k_scatter_rows then writes T back).  Heavy rows as in k_gs.
 template <int KC>
-__global__ void __launch_bounds__(kThreads) k_jacobi_rows(const int32_t* __restrict__ rows, int cnt,
-                                                          const int64_t* __restrict__ rp,
-                                                          const int32_t* __restrict__ col,
-                                                          const double* __restrict__ val,
-                                                          const double* __restrict__ diag,
-                                                          const double* __restrict__ B,
-                                                          const double* __restrict__ X,
-                                                          double* __restrict__ T, HeavyDev H) {
+__global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : kGatherCtas)) k_jacobi_rows(
+    const int32_t* __restrict__ rows, int base, int cnt, const int64_t* __restrict__ rp,
+    const int32_t* __restrict__ col, const double* __restrict__ val,
+    const double* __restrict__ diag, const double* __restrict__ B, const double* __restrict__ X,
+    double* __restrict__ T, HeavyDev H, SegWork w) {
     CF_LANE_SETUP(KC)
     int64_t g = (int64_t)blockIdx.x * Lt::RPB + slot;
-    if (g >= cnt || !lane_ok) return;
-    int64_t i = rows[g];
+    if (!lane_ok) return;
+    int64_t i, q;
     DV<V> acc;
     zero(acc);
-    row_sum<KC, G_PLAIN>(H, i, col, val, rp[i], rp[i + 1], nullptr, nullptr, X, c0, acc);
+    if (g < cnt) {
+        i = rows ? (int64_t)rows[g] : base + g;
+        q = g;
+        const int64_t beg = rp[i], end = rp[i + 1];
+        if (H.hv && end - beg > kHeavyNnz) return;
+        DV<V> b = ldv<V>(B + i * KC + c0);
+        const double d = diag[i];
+        gather_row<KC, G_PLAIN>(col, val, beg, end, nullptr, nullptr, X, c0, acc);
+#pragma unroll
+        for (int t = 0; t < V; ++t) acc.v[t] = (b.v[t] - acc.v[t]) / d;
+        stv<V>(T + q * KC + c0, acc);
+        return;
+    }
+    int64_t s = w.s_lo + (g - cnt);
+    if (s >= w.s_hi) return;
+    int hv;
+    if (!seg_item<KC>(w, s, col, val, X, c0, hv, acc)) return;
+    i = w.h_row[hv];
+    q = w.h_pos[hv] - base;
     DV<V> b = ldv<V>(B + i * KC + c0);
     double d = diag[i];
 #pragma unroll
     for (int t = 0; t < V; ++t) acc.v[t] = (b.v[t] - acc.v[t]) / d;
-    stv<V>(T + g * KC + c0, acc);
+    stv<V>(T + q * KC + c0, acc);
 }
 
 template <int KC>
 __global__ void __launch_bounds__(kThreads) k_scatter_rows(const int32_t* __restrict__ rows,
-                                                           int cnt, const double* __restrict__ T,
+                                                           int base, int cnt,
+                                                           const double* __restrict__ T,
                                                            double* __restrict__ X) {
     CF_LANE_SETUP(KC)
     int64_t g = (int64_t)blockIdx.x * Lt::RPB + slot;
     if (g >= cnt || !lane_ok) return;
-    stv<V>(X + (size_t)rows[g] * KC + c0, ldv<V>(T + g * KC + c0));
+    const int64_t i = rows ? (int64_t)rows[g] : base + g;
+    stv<V>(X + (size_t)i * KC + c0, ldv<V>(T + g * KC + c0));
 }
 
 // bc[a] = sum_{i in a} (b_i - L_i x)  (residual fused with P^T, solver.py:548-549)
 template <int KC>
-__global__ void __launch_bounds__(kThreads) k_agg_restrict(
+__global__ void __launch_bounds__(kThreads, 2) k_agg_restrict(
     int nc, const int32_t* __restrict__ aptr, const int32_t* __restrict__ amem,
     const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
     const double* __restrict__ val, const double* __restrict__ diag,
@@ -389,7 +434,7 @@ __global__ void __launch_bounds__(kThreads) k_agg_restrict(
 // Line-search partials (solver.py:550-556): den = d . L d with d = P xc over
 // fine rows (CTAs [0, pf)), num = r . d = bc . xc over coarse rows (CTAs [pf, pf+pc)).
 template <int KC>
-__global__ void __launch_bounds__(kThreads) k_agg_ls(
+__global__ void __launch_bounds__(kThreads, 2) k_agg_ls(
     int n, int nc, const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
     const double* __restrict__ val, const double* __restrict__ diag,
     const int32_t* __restrict__ agg, const double* __restrict__ Xc,
@@ -451,7 +496,7 @@ __global__ void __launch_bounds__(kThreads) k_agg_correct(int n, const int32_t* 
 
 // bc_i = b[c_i] + sum_f W_cf(i,f) * (b_f / d_f)  (solver.py:534-536)
 template <int KC>
-__global__ void __launch_bounds__(kThreads) k_elim_restrict(
+__global__ void __launch_bounds__(kThreads, 2) k_elim_restrict(
     int nc, const int32_t* __restrict__ cn, const int64_t* __restrict__ wp,
     const int32_t* __restrict__ wc, const double* __restrict__ wv,
     const int32_t* __restrict__ fn, const double* __restrict__ fd,
@@ -470,7 +515,7 @@ __global__ void __launch_bounds__(kThreads) k_elim_restrict(
 
 // Partial sums of heavy-row segments: P[s] = sum over [sbeg[s], send[s]).
 template <int KC, int MODE>
-__global__ void __launch_bounds__(kThreads) k_seg(int64_t s_lo, int64_t s_hi,
+__global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : kGatherCtas)) k_seg(int64_t s_lo, int64_t s_hi,
                                                   const int64_t* __restrict__ sbeg,
                                                   const int64_t* __restrict__ send,
                                                   const int32_t* __restrict__ col,
@@ -490,7 +535,7 @@ __global__ void __launch_bounds__(kThreads) k_seg(int64_t s_lo, int64_t s_hi,
 
 // x[c_i] = xc_i ; x[f] = (b_f + sum W_fc xc) / d_f   (solver.py:538-541)
 template <int KC>
-__global__ void __launch_bounds__(kThreads) k_elim_interp(
+__global__ void __launch_bounds__(kThreads, 2) k_elim_interp(
     int nf, int nc, const int32_t* __restrict__ cn, const int32_t* __restrict__ fn,
     const int64_t* __restrict__ wp, const int32_t* __restrict__ wc,
     const double* __restrict__ wv, const double* __restrict__ fd,
@@ -573,16 +618,65 @@ __global__ void __launch_bounds__(kThreads) k_dense(int n, const double* __restr
     }
 }
 
+// Wide blocks (KC >= 64): 64 x 64 output tiles (column-split grid), 4 x 4
+// register tile per thread, 32-deep l stages; same per-output fma order.
+constexpr int kDT = 64, kDL = 32;
+template <int KC>
+__global__ void __launch_bounds__(kThreads) k_dense_wide(int n, const double* __restrict__ M,
+                                                         const double* __restrict__ B,
+                                                         double* __restrict__ X) {
+    __shared__ double sA[kDL][kDT + 2];
+    __shared__ double sB[kDL][kDT];
+    const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+    const int i0 = blockIdx.x * kDT, j0 = blockIdx.y * kDT;
+    double acc[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+    for (int l0 = 0; l0 < n; l0 += kDL) {
+        for (int e = tid; e < kDT * kDL; e += kThreads) {
+            int r = e / kDL, t = e % kDL;
+            sA[t][r] = (i0 + r < n && l0 + t < n) ? M[(size_t)(i0 + r) * n + l0 + t] : 0.0;
+            int tb = e / kDT, cb = e % kDT;
+            sB[tb][cb] = (l0 + tb < n) ? B[(size_t)(l0 + tb) * KC + j0 + cb] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int t = 0; t < kDL; ++t) {
+            double a[4], bb[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) a[r] = sA[t][ty * 4 + r];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) bb[c] = sB[t][tx + 16 * c];
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) acc[r][c] = fma(a[r], bb[c], acc[r][c]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        int i = i0 + ty * 4 + r;
+        if (i < n)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) X[(size_t)i * KC + j0 + tx + 16 * c] = acc[r][c];
+    }
+}
+
 // rows layout (cnt x n) -> block (n x KC), zero padding for columns >= cnt
+// device row i holds node perm[i] (perm == nullptr: identity)
 template <int KC>
 __global__ void k_rows_to_block(const double* __restrict__ S, int cnt, int n,
-                                double* __restrict__ B) {
+                                const int32_t* __restrict__ perm, double* __restrict__ B) {
     __shared__ double tile[32][33];
     int i0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
     int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
     for (int r = ty; r < 32; r += 8) {
         int c = c0 + r, i = i0 + tx;
-        tile[r][tx] = (c < cnt && i < n) ? S[(size_t)c * n + i] : 0.0;
+        int src = (i < n) ? (perm ? perm[i] : i) : 0;
+        tile[r][tx] = (c < cnt && i < n) ? S[(size_t)c * n + src] : 0.0;
     }
     __syncthreads();
     for (int r = ty; r < 32; r += 8) {
@@ -593,7 +687,7 @@ __global__ void k_rows_to_block(const double* __restrict__ S, int cnt, int n,
 
 template <int KC>
 __global__ void k_block_to_rows(const double* __restrict__ B, int cnt, int n,
-                                double* __restrict__ S) {
+                                const int32_t* __restrict__ perm, double* __restrict__ S) {
     __shared__ double tile[32][33];
     int i0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
     int tx = threadIdx.x, ty = threadIdx.y;
@@ -604,8 +698,24 @@ __global__ void k_block_to_rows(const double* __restrict__ B, int cnt, int n,
     __syncthreads();
     for (int r = ty; r < 32; r += 8) {
         int c = c0 + r, i = i0 + tx;
-        if (c < cnt && i < n) S[(size_t)c * n + i] = tile[tx][r];
+        if (c < cnt && i < n) S[(size_t)c * n + (perm ? perm[i] : i)] = tile[tx][r];
     }
+}
+
+// dst[i, :k] = src[perm[i], :k] (gather, to_dev) or dst[perm[i], :k] = src[i, :k]
+// (scatter); src / dst row strides ks / kd.
+__global__ void k_permute_rows(const double* __restrict__ src, int ks, double* __restrict__ dst,
+                               int kd, int k, int n, const int32_t* __restrict__ perm,
+                               int gather) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (int64_t)n * k) return;
+    int64_t i = t / k;
+    int c = (int)(t % k);
+    int64_t p = perm ? perm[i] : i;
+    if (gather)
+        dst[i * kd + c] = src[p * ks + c];
+    else
+        dst[p * kd + c] = src[i * ks + c];
 }
 
 // ============================================================================
@@ -626,7 +736,15 @@ template <int KC>
 static void finalize(Hier& h, const double* parts, int64_t nparts, int nq, int64_t qstride,
                      double* out) {
     ProfScope ps(h, "finalize", -1, 8.0 * KC * nq * (nparts + 1));
-    k_finalize<KC><<<nq, kThreads, 0, h.s>>>(parts, nparts, qstride, out);
+    const unsigned thr = KC < 32 ? 32 : (KC > kThreads ? kThreads : KC);
+    if (nparts <= kFinSeg) {
+        k_fin2<KC><<<nq, thr, 0, h.s>>>(parts, nparts, qstride, out);
+    } else {
+        const int64_t nseg = (nparts + kFinSeg - 1) / kFinSeg;
+        k_fin1<KC><<<dim3((unsigned)nseg, nq), thr, 0, h.s>>>(parts, nparts, qstride, h.fin,
+                                                              nseg);
+        k_fin2<KC><<<nq, thr, 0, h.s>>>(h.fin, nseg, nseg * KC, out);
+    }
 }
 
 template <int KC>
@@ -641,6 +759,21 @@ struct Ops {
             d.P = h.SP;
         }
         return d;
+    }
+    static SegWork segwork(const Hier& h, const Plan& pl, int64_t lo, int64_t hi) {
+        SegWork w;
+        if (!pl.nheavy || hi <= lo) return w;
+        w.s_lo = lo;
+        w.s_hi = hi;
+        w.sbeg = pl.sbeg;
+        w.send = pl.send;
+        w.seg_hv = pl.seg_hv;
+        w.hsp = pl.hsp;
+        w.h_row = pl.h_row;
+        w.h_pos = pl.h_pos;
+        w.cntr = pl.cntr;
+        w.SP = h.SP;
+        return w;
     }
     // segment partials of a plan's segments [lo, hi)
     template <int MODE>
@@ -707,8 +840,13 @@ struct Ops {
                 CF_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * (size_t)l.n * KC, h.s));
             } else {
                 ProfScope ps(h, "dense", j, 8.0 * l.n * l.n + 2 * Vb(l.n));
-                k_dense<KC><<<(unsigned)((l.n + kDenseTR - 1) / kDenseTR), kThreads, 0, h.s>>>(
-                    l.n, l.M, b, x);
+                if constexpr (KC >= 64) {
+                    dim3 grd((unsigned)((l.n + kDT - 1) / kDT), KC / kDT);
+                    k_dense_wide<KC><<<grd, kThreads, 0, h.s>>>(l.n, l.M, b, x);
+                } else {
+                    k_dense<KC><<<(unsigned)((l.n + kDenseTR - 1) / kDenseTR), kThreads, 0,
+                                  h.s>>>(l.n, l.M, b, x);
+                }
             }
             return;
         }
@@ -771,15 +909,14 @@ struct Ops {
         int beg = l.cptr[colr], cnt = l.cptr[colr + 1] - beg;
         if (cnt <= 0) return;
         const int lev = (int)(&l - &h.L[0]);
-        if (!from_zero)
-            seg<G_PLAIN>(h, l.pm, l.pm.cseg[colr], l.pm.cseg[colr + 1], l.col, l.val, nullptr,
-                         nullptr, x, lev);
+        SegWork w = segwork(h, l.pm, from_zero ? 0 : l.pm.cseg[colr],
+                            from_zero ? 0 : l.pm.cseg[colr + 1]);
         ProfScope ps(h, "gs_sweep", lev,
                      12.0 * l.c_nnz[colr] + 20.0 * cnt +
                          Vb(2 * cnt + (from_zero ? 0 : l.c_nbr[colr])));
-        k_gs<KC><<<grid_rows<KC>(cnt), kThreads, 0, h.s>>>(l.crows + beg, cnt, l.rp, l.col, l.val,
-                                                         l.diag, b, x, from_zero ? 1 : 0,
-                                                         hd(h, l.pm));
+        k_gs<KC><<<grid_rows<KC>(cnt + (w.s_hi - w.s_lo)), kThreads, 0, h.s>>>(
+            l.contig ? nullptr : l.crows + beg, beg, cnt, l.rp, l.col, l.val, l.diag, b, x,
+            from_zero ? 1 : 0, hd(h, l.pm), w);
     }
 
     static void jacobi(Hier& h, DLevel& l, const double* b, double* x) {
@@ -787,8 +924,7 @@ struct Ops {
         int beg = l.cptr[K], cnt = l.cptr[l.ncolors] - beg;
         if (cnt <= 0) return;
         const int lev = (int)(&l - &h.L[0]);
-        seg<G_PLAIN>(h, l.pm, l.pm.cseg[K], l.pm.cseg[l.ncolors], l.col, l.val, nullptr, nullptr,
-                     x, lev);
+        SegWork w = segwork(h, l.pm, l.pm.cseg[K], l.pm.cseg[l.ncolors]);
         int64_t nnz = 0, nbr = 0;
         for (int c = K; c < l.ncolors; ++c) {
             nnz += l.c_nnz[c];
@@ -796,11 +932,13 @@ struct Ops {
         }
         {
             ProfScope ps(h, "jacobi_merged", lev, 12.0 * nnz + 20.0 * cnt + Vb(2 * cnt + nbr));
-            k_jacobi_rows<KC><<<grid_rows<KC>(cnt), kThreads, 0, h.s>>>(
-                l.crows + beg, cnt, l.rp, l.col, l.val, l.diag, b, x, h.T, hd(h, l.pm));
+            k_jacobi_rows<KC><<<grid_rows<KC>(cnt + (w.s_hi - w.s_lo)), kThreads, 0, h.s>>>(
+                l.contig ? nullptr : l.crows + beg, beg, cnt, l.rp, l.col, l.val, l.diag, b, x,
+                h.T, hd(h, l.pm), w);
         }
         ProfScope ps(h, "jacobi_scatter", lev, Vb(2 * cnt) + 4.0 * cnt);
-        k_scatter_rows<KC><<<grid_rows<KC>(cnt), kThreads, 0, h.s>>>(l.crows + beg, cnt, h.T, x);
+        k_scatter_rows<KC><<<grid_rows<KC>(cnt), kThreads, 0, h.s>>>(
+            l.contig ? nullptr : l.crows + beg, beg, cnt, h.T, x);
     }
 
     static void run_cycle(Hier& h, int nu1, int nu2) {
@@ -1242,12 +1380,12 @@ void solve_block(Hier& h, int kc, int ncols, const CfSolveParams& p, double* res
 void rows_to_block(Hier& h, const double* S_dev, int cnt, int kc, double* B_dev) {
     dim3 blk(32, 8), grd((h.n0 + 31) / 32, (kc + 31) / 32);
     ProfScope ps(h, "transpose", 0, 16.0 * kc * h.n0);
-    CF_DISPATCH(kc, (k_rows_to_block<K_><<<grd, blk, 0, h.s>>>(S_dev, cnt, h.n0, B_dev)));
+    CF_DISPATCH(kc, (k_rows_to_block<K_><<<grd, blk, 0, h.s>>>(S_dev, cnt, h.n0, h.perm0, B_dev)));
 }
 void block_to_rows(Hier& h, const double* B_dev, int cnt, int kc, double* S_dev) {
     dim3 blk(32, 8), grd((h.n0 + 31) / 32, (kc + 31) / 32);
     ProfScope ps(h, "transpose", 0, 16.0 * kc * h.n0);
-    CF_DISPATCH(kc, (k_block_to_rows<K_><<<grd, blk, 0, h.s>>>(B_dev, cnt, h.n0, S_dev)));
+    CF_DISPATCH(kc, (k_block_to_rows<K_><<<grd, blk, 0, h.s>>>(B_dev, cnt, h.n0, h.perm0, S_dev)));
 }
 void finalize_dev(Hier& h, const double* parts, int64_t nparts, int nq, int64_t qstride,
                   double* out, int kc) {
@@ -1287,6 +1425,7 @@ Hier::~Hier() {
     cudaFree(P);
     cudaFree(AP);
     cudaFree(parts);
+    cudaFree(fin);
     cudaFree(SP);
     cudaFree(T);
     cudaFree(S);
@@ -1322,6 +1461,7 @@ void Hier::ensure_workspace(int kc) {
     re(parts, np * kc);
     parts_cap = np * kc;
     re(SP, (size_t)std::max<int64_t>(max_nseg, 1) * kc);
+    re(fin, (size_t)(3 * (np / kFinSeg + 2)) * kc);
     re(T, (size_t)std::max<int64_t>(max_merged, 1) * kc);
     if (Z) {
         cudaFree(Z); cudaFree(P); cudaFree(AP);
@@ -1385,7 +1525,7 @@ static T* upload(Hier& h, const T* src, size_t cnt);
 static Plan build_plan(Hier& h, int64_t n, const int64_t* rp, const int32_t* order,
                        const int32_t* cls_ptr, int ncls) {
     Plan pl;
-    std::vector<int32_t> hv(n, -1);
+    std::vector<int32_t> hv(n, -1), shv, hrow, hpos;
     std::vector<int64_t> hsp{0}, sb, se;
     if (!order) ncls = 1;
     for (int c = 0; c < ncls; ++c) {
@@ -1395,11 +1535,15 @@ static Plan build_plan(Hier& h, int64_t n, const int64_t* rp, const int32_t* ord
             int64_t i = order ? order[q] : q;
             int64_t deg = rp[i + 1] - rp[i];
             if (deg <= kHeavyNnz) continue;
-            hv[i] = (int32_t)pl.nheavy++;
+            hv[i] = (int32_t)pl.nheavy;
+            hrow.push_back((int32_t)i);
+            hpos.push_back((int32_t)q);
             for (int64_t b = rp[i]; b < rp[i + 1]; b += kSegNnz) {
                 sb.push_back(b);
                 se.push_back(std::min<int64_t>(b + kSegNnz, rp[i + 1]));
+                shv.push_back((int32_t)pl.nheavy);
             }
+            pl.nheavy++;
             hsp.push_back((int64_t)sb.size());
         }
     }
@@ -1410,6 +1554,11 @@ static Plan build_plan(Hier& h, int64_t n, const int64_t* rp, const int32_t* ord
         pl.hsp = upload(h, hsp.data(), hsp.size());
         pl.sbeg = upload(h, sb.data(), sb.size());
         pl.send = upload(h, se.data(), se.size());
+        pl.seg_hv = upload(h, shv.data(), shv.size());
+        pl.h_row = upload(h, hrow.data(), hrow.size());
+        pl.h_pos = upload(h, hpos.data(), hpos.size());
+        pl.cntr = (int*)h.dalloc(sizeof(int) * pl.nheavy);
+        CF_CUDA(cudaMemset(pl.cntr, 0, sizeof(int) * pl.nheavy));
     }
     h.max_nseg = std::max(h.max_nseg, pl.nseg);
     return pl;
@@ -1465,6 +1614,8 @@ extern "C" int cf_hier_create(int32_t nlev, const CfLevelDesc* ds, int32_t devic
                         h->max_merged, d.color_ptr[d.n_colors] - d.color_ptr[kGsClasses]);
                 l.cptr.assign(d.color_ptr, d.color_ptr + d.n_colors + 1);
                 l.crows = upload(*h, d.color_rows, (size_t)d.n);
+                l.contig = true;
+                for (int32_t q = 0; q < d.n && l.contig; ++q) l.contig = d.color_rows[q] == q;
                 l.agg = upload(*h, d.agg, (size_t)d.n);
                 l.aptr = upload(*h, d.agg_ptr, (size_t)d.n_coarse + 1);
                 l.amem = upload(*h, d.agg_members, (size_t)d.n);
@@ -1578,14 +1729,15 @@ extern "C" int cf_solve_block_dev(void* hp, const double* B_dev, double* X_dev, 
     if (k < 1 || k > kMaxKC) throw CfError(CF_DOMAIN, "k must be in [1, 256]");
     int kc = kc_at_least(k);
     h.ensure_workspace(kc);
-    // B_dev is n x k row-major; widen to kc columns
+    // B_dev is n x k row-major in node order; widen to kc columns in device order
     CF_CUDA(cudaMemsetAsync(h.B, 0, sizeof(double) * (size_t)h.n0 * kc, h.s));
-    CF_CUDA(cudaMemcpy2DAsync(h.B, sizeof(double) * kc, B_dev, sizeof(double) * k,
-                              sizeof(double) * k, h.n0, cudaMemcpyDeviceToDevice, h.s));
+    int64_t tot = (int64_t)h.n0 * k;
+    k_permute_rows<<<(unsigned)((tot + 255) / 256), 256, 0, h.s>>>(B_dev, k, h.B, kc, k, h.n0,
+                                                                     h.perm0, 1);
     std::vector<double> res(kc, 0.0);
     solve_block(h, kc, k, *p, res.data(), *st);
-    CF_CUDA(cudaMemcpy2DAsync(X_dev, sizeof(double) * k, h.X, sizeof(double) * kc,
-                              sizeof(double) * k, h.n0, cudaMemcpyDeviceToDevice, h.s));
+    k_permute_rows<<<(unsigned)((tot + 255) / 256), 256, 0, h.s>>>(h.X, kc, X_dev, k, k, h.n0,
+                                                                     h.perm0, 0);
     CF_CUDA(cudaStreamSynchronize(h.s));
     std::memcpy(residuals, res.data(), sizeof(double) * k);
     CF_API_END_STATS(st)
@@ -1600,7 +1752,12 @@ extern "C" int cf_residual_dev(void* hp, const double* B_dev, const double* X_de
     int kc = pick_kc(k);
     if (kc != k) throw CfError(CF_DOMAIN, "k must be a supported block width");
     h.ensure_workspace(kc);
-    CF_DISPATCH(kc, Ops<K_>::residual(h, B_dev, X_dev, R_dev, h.sums));
+    int64_t tot = (int64_t)h.n0 * k;
+    unsigned grd = (unsigned)((tot + 255) / 256);
+    k_permute_rows<<<grd, 256, 0, h.s>>>(B_dev, k, h.B, kc, k, h.n0, h.perm0, 1);
+    k_permute_rows<<<grd, 256, 0, h.s>>>(X_dev, k, h.X, kc, k, h.n0, h.perm0, 1);
+    CF_DISPATCH(kc, Ops<K_>::residual(h, h.B, h.X, h.R, h.sums));
+    k_permute_rows<<<grd, 256, 0, h.s>>>(h.R, kc, R_dev, k, k, h.n0, h.perm0, 0);
     CF_CUDA(cudaMemcpyAsync(colsq, h.sums + k, sizeof(double) * k, cudaMemcpyDeviceToHost, h.s));
     CF_CUDA(cudaStreamSynchronize(h.s));
     CF_API_END
@@ -1652,5 +1809,16 @@ extern "C" int cf_profile_report(void* hp, char* buf, int64_t cap, int64_t* need
         std::memcpy(buf, out.data(), nb);
         buf[nb] = 0;
     }
+    CF_API_END
+}
+
+extern "C" int cf_hier_set_order(void* hp, const int32_t* perm, int64_t n) {
+    CF_API_BEGIN
+    Hier& h = *(Hier*)hp;
+    std::lock_guard<std::mutex> lk(h.mu);
+    CF_CUDA(cudaSetDevice(h.dev));
+    if (n != h.n0) throw CfError(CF_DOMAIN, "order length does not match the hierarchy");
+    if (!h.perm0) h.perm0 = (int32_t*)h.dalloc(sizeof(int32_t) * std::max<int64_t>(n, 1));
+    CF_CUDA(cudaMemcpy(h.perm0, perm, sizeof(int32_t) * n, cudaMemcpyHostToDevice));
     CF_API_END
 }

@@ -78,7 +78,7 @@ def _node_solve(hierarchy: MultigridHierarchy, nodes: np.ndarray, config: Solver
         return sub, z, res
     dev = hierarchy.device()
     st = N.CfSolveStats()
-    nd = np.ascontiguousarray(nodes, dtype=np.int64)
+    nd = np.ascontiguousarray(dev.inv0[np.asarray(nodes, dtype=np.int64)], dtype=np.int64)
     N.check(N.lib().cf_node_solutions(dev.handle, N.ptr(nd, N.i64p), cnt,
                                       N.C.byref(_params(config, n)), N.ptr(sub, N.f64p),
                                       N.ptr(z, N.f64p), N.ptr(res, N.f64p), N.C.byref(st)), st)
@@ -163,9 +163,15 @@ class _DeviceGraph:
     def __init__(self, g: Graph, hierarchy: MultigridHierarchy):
         eid, sqw = edge_index_view(g)
         self._h = hierarchy.device()
-        ap = np.ascontiguousarray(g.indptr, dtype=np.int64)
-        nb = np.ascontiguousarray(g.indices, dtype=np.int32)
-        ei = np.ascontiguousarray(eid, dtype=np.int32)
+        # adjacency rows in device order (row i' = node perm0[i']), entries of
+        # each row kept in ascending canonical edge order
+        perm0 = self._h.perm0
+        deg = np.diff(g.indptr)[perm0]
+        ap = np.zeros(g.n + 1, dtype=np.int64)
+        np.cumsum(deg, out=ap[1:])
+        src = np.repeat(g.indptr[:-1][perm0] - ap[:-1], deg) + np.arange(ap[-1])
+        nb = np.ascontiguousarray(g.indices[src], dtype=np.int32)
+        ei = np.ascontiguousarray(eid[src], dtype=np.int32)
         sw = np.ascontiguousarray(sqw, dtype=np.float64)
         h = N.C.c_void_p()
         N.check(N.lib().cf_graph_create(self._h.handle, g.n, sw.size, N.ptr(ap, N.i64p),
@@ -212,7 +218,8 @@ def _sketch_device(g: Graph, hierarchy: MultigridHierarchy, epsilon: float, seed
     k = sketch_dimension(n, epsilon)
     r0, r1 = (0, k) if rows is None else rows
     dg = _device_graph(g, hierarchy)
-    q = np.zeros(0, dtype=np.int64) if query is None else np.ascontiguousarray(query, np.int64)
+    q = np.zeros(0, dtype=np.int64) if query is None else np.asarray(query, np.int64)
+    q = np.ascontiguousarray(hierarchy.device().inv0[q], dtype=np.int64)
     sums = np.zeros(max(q.size, 1))
     z = np.empty((r1 - r0, n)) if want_z else None
     res = np.zeros(r1 - r0)

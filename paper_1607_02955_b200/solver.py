@@ -61,6 +61,10 @@ STOP_MARGIN = 0.9
 # V-cycle) instead of recursing through the deep tail of tiny levels.
 DEVICE_DIRECT_MAX = 4096
 DEVICE_DIRECT_FRACTION = 1.0 / 16.0
+# Locality ordering of the device copy: every non-dense level is
+# renumbered by reverse Cuthill-McKee so neighbour gathers of the row-major
+# blocks hit L2; the permutation is applied at the API boundary.
+DEVICE_REORDER = True
 
 
 @dataclass(frozen=True)
@@ -167,6 +171,61 @@ def device_levels(levels: list[Level]) -> list[Level]:
     return list(levels)
 
 
+def _identity(n):
+    return np.arange(n, dtype=np.int64)
+
+
+def permute_levels(levels: list[Level]):
+    """Renumber each non-dense level by RCM; returns (levels', perm0) with
+    perm0[i'] = original node of device row i' on level 0.  Transfer
+    operators are remapped so the permuted hierarchy is the same operator."""
+    from scipy.sparse.csgraph import reverse_cuthill_mckee
+
+    perms, classes = [], []
+    for lvl in levels:
+        classes.append(None)
+        if lvl.kind is LevelKind.COARSEST or not DEVICE_REORDER:
+            perms.append(_identity(lvl.size))
+            continue
+        A = lvl.matrix.tocsr()
+        p = np.asarray(reverse_cuthill_mckee(A, symmetric_mode=True), dtype=np.int64)
+        if lvl.kind is LevelKind.AGGREGATION:
+            # colour classes of the RCM-ordered matrix become contiguous row
+            # ranges (RCM order kept inside each class)
+            col = _colour(A[p][:, p].tocsr())
+            order = np.argsort(col, kind="stable")
+            p = p[order]
+            classes[-1] = col[order]
+        perms.append(p)
+    invs = []
+    for p in perms:
+        inv = np.empty_like(p)
+        inv[p] = np.arange(p.size)
+        invs.append(inv)
+    out = []
+    for j, lvl in enumerate(levels):
+        p, inv = perms[j], invs[j]
+        if lvl.kind is LevelKind.COARSEST:
+            out.append(lvl)
+            continue
+        A = lvl.matrix.tocsr()[p][:, p].tocsr()
+        A.sort_indices()
+        pn, invn = perms[j + 1], invs[j + 1]
+        if lvl.kind is LevelKind.AGGREGATION:
+            agg = invn[lvl.aggregates[p]]
+            col = classes[j] if classes[j] is not None else _colour(A)
+            out.append(Level(kind=LevelKind.AGGREGATION, matrix=A, aggregates=agg, colors=col))
+        else:
+            f_new = inv[lvl.f_nodes]
+            order = np.argsort(f_new, kind="stable")
+            w_cf = lvl.w_cf.tocsr()[pn][:, order].tocsr()
+            w_cf.sort_indices()
+            out.append(Level(kind=LevelKind.ELIMINATION, matrix=A, f_nodes=f_new[order],
+                             c_nodes=inv[lvl.c_nodes[pn]], f_degree=lvl.f_degree[order],
+                             w_cf=w_cf, w_fc=w_cf.T.tocsr()))
+    return out, perms[0]
+
+
 class _DeviceHierarchy:
     """Owner of the C handle (device operators + workspace)."""
 
@@ -177,14 +236,19 @@ class _DeviceHierarchy:
             raise RuntimeError("cfcent_b200: no CUDA device visible; the solve path has no "
                                "CPU fallback")
         self._keep = []
-        levels = device_levels(levels)
+        levels, perm0 = permute_levels(device_levels(levels))
         self.levels = levels
+        self.perm0 = perm0                       # device row -> node
+        self.inv0 = np.empty_like(perm0)         # node -> device row
+        self.inv0[perm0] = np.arange(perm0.size)
         descs = (N.CfLevelDesc * len(levels))()
         for j, lvl in enumerate(levels):
             self._fill(descs[j], lvl, j)
         h = N.C.c_void_p()
         N.check(L.cf_hier_create(len(levels), descs, device, N.C.byref(h)))
         self.handle = h
+        p32 = np.ascontiguousarray(perm0, dtype=np.int32)
+        N.check(L.cf_hier_set_order(h, N.ptr(p32, N.i32p), p32.size))
         self._keep = None  # host arrays were copied to the device
 
     def _arr(self, a, dt):
