@@ -181,9 +181,12 @@ int cf_profile_report(void* handle, char* buf, int64_t cap, int64_t* needed);
  * <= cap; writes chosen ids to out_f, returns the count in *n_f. */
 int cf_setup_elim_select(int64_t n, const int64_t* indptr, const int64_t* indices,
                          int32_t cap, int64_t* out_f, int64_t* n_f);
-/* solver.py:297-346: seeds + affinity attachment, aggregate map in out_agg. */
+/* solver.py:297-346: seeds + affinity attachment with aggregate size cap
+ * (8 in the reference) and affinity threshold (0.5 in the reference),
+ * aggregate map in out_agg. */
 int cf_setup_aggregate(int64_t n, const int64_t* indptr, const int64_t* indices,
-                       const double* tv, int32_t n_tv, int64_t* out_agg, int64_t* n_agg);
+                       const double* tv, int32_t n_tv, int32_t cap, double threshold,
+                       int64_t* out_agg, int64_t* n_agg);
 /* solver.py:364-380: greedy matching over a pre-sorted edge order. */
 int cf_setup_matching(int64_t n, int64_t n_edges, const int64_t* eu, const int64_t* ev,
                       const int64_t* order, int64_t* out_agg, int64_t* n_agg);

@@ -88,7 +88,8 @@ _SIGS = {
     "cf_profile": (C.c_int, [C.c_void_p, C.c_int32]),
     "cf_profile_report": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int64, i64p]),
     "cf_setup_elim_select": (C.c_int, [C.c_int64, i64p, i64p, C.c_int32, i64p, i64p]),
-    "cf_setup_aggregate": (C.c_int, [C.c_int64, i64p, i64p, f64p, C.c_int32, i64p, i64p]),
+    "cf_setup_aggregate": (C.c_int, [C.c_int64, i64p, i64p, f64p, C.c_int32, C.c_int32,
+                                     C.c_double, i64p, i64p]),
     "cf_setup_matching": (C.c_int, [C.c_int64, C.c_int64, i64p, i64p, i64p, i64p, i64p]),
     "cf_setup_colour": (C.c_int, [C.c_int64, i64p, i64p, i32p, i32p]),
 }

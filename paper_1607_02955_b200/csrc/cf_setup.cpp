@@ -33,11 +33,13 @@ extern "C" int cf_setup_elim_select(int64_t n, const int64_t* indptr, const int6
 }
 
 extern "C" int cf_setup_aggregate(int64_t n, const int64_t* indptr, const int64_t* indices,
-                                  const double* tv, int32_t nt, int64_t* out_agg,
-                                  int64_t* n_agg) {
+                                  const double* tv, int32_t nt, int32_t cap, double threshold,
+                                  int64_t* out_agg, int64_t* n_agg) {
     // solver.py:297-346.  Affinity of u,v: <x_u,x_v>^2 / (|x_u|^2 |x_v|^2).
-    const double kThreshold = 0.5;
-    const int kCap = 8, kPasses = 3;
+    // cap = MAX_AGGREGATE_SIZE (8) reproduces the reference; the stall breaker
+    // of the B200 setup retries with larger caps.
+    const double kThreshold = threshold;  // AFFINITY_THRESHOLD = 0.5 in the reference
+    const int kCap = cap, kPasses = 3;
     std::vector<double> nrm(n);
     for (int64_t i = 0; i < n; ++i) {
         double s = 0.0;

@@ -65,6 +65,18 @@ DEVICE_DIRECT_FRACTION = 1.0 / 16.0
 # renumbered by reverse Cuthill-McKee so neighbour gathers of the row-major
 # blocks hit L2; the permutation is applied at the API boundary.
 DEVICE_REORDER = True
+# Stall breaker (B200 setup): on power-law graphs the reference's
+# stages shrink a level by ~0.01-1 % for thousands of levels (R-MAT scale 20:
+# 2,859 levels).  When both reference stages miss MIN_REDUCTION, the setup
+# also tries exact elimination with off-degree cap STALL_ELIM_CAP and affinity
+# aggregation with cap STALL_AGG_CAP / threshold STALL_AGG_THRESHOLD, and keeps
+# the largest reduction.  Active on levels above DEVICE_DIRECT_MAX nodes, or on
+# every level when n0 > STALL_BREAKER_MIN_N0; graphs whose hierarchies never
+# stall there (C1-C3) keep the reference hierarchy exactly.
+STALL_ELIM_CAP = 16
+STALL_AGG_CAP = 64
+STALL_AGG_THRESHOLD = 0.0
+STALL_BREAKER_MIN_N0 = 262144
 
 
 @dataclass(frozen=True)
@@ -482,9 +494,11 @@ def _galerkin(matrix: sp.csr_matrix, agg: np.ndarray, n_agg: int) -> sp.csr_matr
     return _rebuild_laplacian(p.T @ matrix @ p)
 
 
-def coarsen_aggregate(matrix: sp.csr_matrix, test_vectors: np.ndarray):
+def coarsen_aggregate(matrix: sp.csr_matrix, test_vectors: np.ndarray,
+                      cap: int = MAX_AGGREGATE_SIZE, threshold: float = AFFINITY_THRESHOLD):
     """Affinity aggregation + Galerkin coarse operator (solver.py:278-346).
-    Returns ``(coarse, aggregates)``."""
+    Returns ``(coarse, aggregates)``.  ``cap`` is the aggregate size limit
+    (the reference's 8 by default)."""
     matrix = matrix.tocsr()
     n = matrix.shape[0]
     ip, ix = _csr64(matrix)
@@ -492,8 +506,8 @@ def coarsen_aggregate(matrix: sp.csr_matrix, test_vectors: np.ndarray):
     agg = np.empty(n, dtype=np.int64)
     na = np.zeros(1, dtype=np.int64)
     N.check(N.lib().cf_setup_aggregate(n, N.ptr(ip, N.i64p), N.ptr(ix, N.i64p),
-                                       N.ptr(tv, N.f64p), tv.shape[1], N.ptr(agg, N.i64p),
-                                       N.ptr(na, N.i64p)))
+                                       N.ptr(tv, N.f64p), tv.shape[1], int(cap),
+                                       float(threshold), N.ptr(agg, N.i64p), N.ptr(na, N.i64p)))
     return _galerkin(matrix, agg, int(na[0])), agg
 
 
@@ -557,19 +571,32 @@ def _coarse_operator(level: Level) -> np.ndarray:
     return m - m.mean(axis=0, keepdims=True)
 
 
-def setup(matrix: sp.spmatrix, config: SolverConfig | None = None) -> MultigridHierarchy:
+def setup(matrix: sp.spmatrix, config: SolverConfig | None = None,
+          stall_breaker: bool | None = None) -> MultigridHierarchy:
     """Build the hierarchy with the reference's stage rule (solver.py:422-523).
 
     Elimination first; a stage shrinking the level by < 10 % yields to the
     other; if neither clears the bar the larger reduction is taken; the
     preferred stage alternates.  The result lives on the host until the first
     solve uploads it to the device.
+
+    ``stall_breaker``: None (default) enables the stall breaker (see
+    STALL_ELIM_CAP) on levels above DEVICE_DIRECT_MAX nodes or on graphs with
+    more than STALL_BREAKER_MIN_N0 nodes; False reproduces the reference rule
+    everywhere; True enables it on every level.
     """
     config = config or SolverConfig()
     current = _validate_laplacian(matrix)
     rng = np.random.default_rng(config.seed)
     levels: list[Level] = []
     preferred = LevelKind.ELIMINATION
+    n0 = current.shape[0]
+    tvecs: dict[int, np.ndarray] = {}
+
+    def breaker_on(n_level: int) -> bool:
+        if stall_breaker is not None:
+            return bool(stall_breaker)
+        return n0 > STALL_BREAKER_MIN_N0 or n_level > DEVICE_DIRECT_MAX
     while current.shape[0] > config.max_direct_size:
         n_cur = current.shape[0]
         need = MIN_REDUCTION * n_cur
@@ -582,6 +609,7 @@ def setup(matrix: sp.spmatrix, config: SolverConfig | None = None) -> MultigridH
                     cand[kind] = (0 if rec is None else rec.f_nodes.size, schur, rec)
                 else:
                     vec = relaxed_test_vectors(current, config.aggregation_test_vectors, rng)
+                    tvecs[n_cur] = vec
                     coarse, agg = coarsen_aggregate(current, vec)
                     red = n_cur - (int(agg.max()) + 1)
                     if red < need:
@@ -595,6 +623,17 @@ def setup(matrix: sp.spmatrix, config: SolverConfig | None = None) -> MultigridH
         other = (LevelKind.AGGREGATION if preferred is LevelKind.ELIMINATION
                  else LevelKind.ELIMINATION)
         applied = next((k for k in (preferred, other) if stage(k)[0] >= need), None)
+        if applied is None and breaker_on(n_cur):
+            stage(LevelKind.AGGREGATION)
+            schur, rec = coarsen_eliminate(current, STALL_ELIM_CAP)
+            alt = {"elim": (0 if rec is None else rec.f_nodes.size, schur, rec)}
+            co, ag = coarsen_aggregate(current, tvecs[n_cur], STALL_AGG_CAP, STALL_AGG_THRESHOLD)
+            alt["agg"] = (n_cur - (int(ag.max()) + 1), co, ag)
+            best = max(alt, key=lambda k: alt[k][0])
+            if alt[best][0] > max(c[0] for c in cand.values()):
+                kind = LevelKind.ELIMINATION if best == "elim" else LevelKind.AGGREGATION
+                cand[kind] = alt[best]
+                applied = kind
         if applied is None:
             applied = max(cand, key=lambda k: cand[k][0])
             if cand[applied][0] <= 0:

@@ -141,3 +141,21 @@ def test_config2_closeness_parity():
         rel = np.abs(jl.vector(q) / d[f"jl_{tag}"] - 1).max()
         assert rel <= tol, (tau, rel)
         assert h.stats.max_residual <= tau
+
+
+def test_jl_rhs_bit_exact_with_hub_nodes():
+    """Nodes above the hub threshold take the CTA-per-hub path; still
+    bit-identical to the reference's ascending-edge sums."""
+    rng = np.random.default_rng(8)
+    n = 6000
+    u = np.r_[np.zeros(n - 1, dtype=np.int64), np.ones(2500, dtype=np.int64),
+              rng.integers(0, n, 3000)]
+    v = np.r_[np.arange(1, n), rng.integers(2, n, 2500), rng.integers(0, n, 3000)]
+    w = rng.uniform(0.5, 2.0, u.size)
+    g = P.Graph.from_edges(u, v, w, n=n)
+    og = O.graph_from_edges(u, v, w, n=n)
+    assert np.diff(g.indptr).max() > 2048
+    h = P.setup(P.laplacian(g))
+    for k in (8, 64, 200):
+        ref, _ = O.jl_rhs(og, k, 5)
+        assert np.array_equal(jl_rhs_rows(g, h, k, 5), ref)
