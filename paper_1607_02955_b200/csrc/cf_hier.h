@@ -113,6 +113,10 @@ struct Hier {
     int prof_begin(const char* kind, int level, double bytes);
     void prof_end(int idx);
 
+    void* stage_host = nullptr;       // pinned staging ring for pageable transfers
+    cudaEvent_t stage_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    void ensure_stage();
+
     ~Hier();
     void* dalloc(size_t bytes_);
     void ensure_workspace(int kc);
@@ -137,6 +141,10 @@ void solve_block(Hier& h, int kc, int ncols, const CfSolveParams& p, double* res
 // Transposes between rows layout (cnt x n) and block layout (n x kc).
 void rows_to_block(Hier& h, const double* S_dev, int cnt, int kc, double* B_dev);
 void block_to_rows(Hier& h, const double* B_dev, int cnt, int kc, double* S_dev);
+// pageable host <-> device copies through the pinned staging ring (sync-free
+// issue on h.s; d2h returns when the host buffer is filled)
+void h2d_staged(Hier& h, void* dst_dev, const void* src_host, size_t bytes);
+void d2h_staged(Hier& h, void* dst_host, const void* src_dev, size_t bytes);
 // Column sums over level-0 n x kc block -> h.sums (device), one quantity.
 void colsum_dev(Hier& h, const double* X_dev, int kc, double* out_dev);
 // out[q*kc + c] = sum_p parts[q*qstride + p*kc + c]

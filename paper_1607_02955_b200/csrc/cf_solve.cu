@@ -16,6 +16,7 @@
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "cf_common.h"
@@ -1430,6 +1431,9 @@ Hier::~Hier() {
     cudaFree(T);
     cudaFree(S);
     if (h_count) cudaFreeHost(h_count);
+    if (stage_host) cudaFreeHost(stage_host);
+    for (auto& e : stage_ev)
+        if (e) cudaEventDestroy(e);
     if (h_small) cudaFreeHost(h_small);
     if (s) cudaStreamDestroy(s);
 }
@@ -1504,6 +1508,82 @@ void Hier::prof_end(int idx) { cudaEventRecord(recs[idx].b, s); }
 }  // namespace cf
 
 using namespace cf;
+
+// ============================================================================
+// Host <-> device transfers of pageable buffers: the bytes go through a
+// persistent pinned staging ring; host-side memcpy is split over threads and
+// overlapped with the DMA of the previous piece.
+// ============================================================================
+
+namespace cf {
+static constexpr size_t kStagePiece = 16u << 20;  // bytes per piece
+static constexpr int kStagePieces = 4;
+
+static void par_memcpy(void* dst, const void* src, size_t bytes) {
+    const size_t kMin = 4u << 20;
+    unsigned nt = std::min<unsigned>(8, std::max<unsigned>(1, (unsigned)(bytes / kMin)));
+    if (nt <= 1) {
+        std::memcpy(dst, src, bytes);
+        return;
+    }
+    std::vector<std::thread> th;
+    size_t per = (bytes + nt - 1) / nt;
+    for (unsigned t = 0; t < nt; ++t) {
+        size_t a = t * per, b = std::min(bytes, a + per);
+        if (a >= b) break;
+        th.emplace_back([=] { std::memcpy((char*)dst + a, (const char*)src + a, b - a); });
+    }
+    for (auto& x : th) x.join();
+}
+
+void Hier::ensure_stage() {
+    if (stage_host) return;
+    CF_CUDA(cudaMallocHost(&stage_host, kStagePiece * kStagePieces));
+    for (int i = 0; i < kStagePieces; ++i) CF_CUDA(cudaEventCreateWithFlags(&stage_ev[i], cudaEventDisableTiming));
+}
+
+void h2d_staged(Hier& h, void* dst_dev, const void* src_host, size_t bytes) {
+    h.ensure_stage();
+    size_t off = 0;
+    int slot = 0;
+    std::vector<bool> used(kStagePieces, false);
+    while (off < bytes) {
+        size_t nb = std::min(kStagePiece, bytes - off);
+        char* st = (char*)h.stage_host + (size_t)slot * kStagePiece;
+        if (used[slot]) CF_CUDA(cudaEventSynchronize(h.stage_ev[slot]));
+        par_memcpy(st, (const char*)src_host + off, nb);
+        CF_CUDA(cudaMemcpyAsync((char*)dst_dev + off, st, nb, cudaMemcpyHostToDevice, h.s));
+        CF_CUDA(cudaEventRecord(h.stage_ev[slot], h.s));
+        used[slot] = true;
+        off += nb;
+        slot = (slot + 1) % kStagePieces;
+    }
+}
+
+void d2h_staged(Hier& h, void* dst_host, const void* src_dev, size_t bytes) {
+    h.ensure_stage();
+    // issue up to kStagePieces DMAs ahead, drain in order
+    const size_t npieces = (bytes + kStagePiece - 1) / kStagePiece;
+    size_t issued = 0, drained = 0;
+    auto issue = [&](size_t k) {
+        size_t off = k * kStagePiece, nb = std::min(kStagePiece, bytes - off);
+        int slot = (int)(k % kStagePieces);
+        CF_CUDA(cudaMemcpyAsync((char*)h.stage_host + (size_t)slot * kStagePiece,
+                                (const char*)src_dev + off, nb, cudaMemcpyDeviceToHost, h.s));
+        CF_CUDA(cudaEventRecord(h.stage_ev[slot], h.s));
+    };
+    while (issued < npieces && issued < (size_t)kStagePieces) issue(issued++);
+    while (drained < npieces) {
+        int slot = (int)(drained % kStagePieces);
+        size_t off = drained * kStagePiece, nb = std::min(kStagePiece, bytes - off);
+        CF_CUDA(cudaEventSynchronize(h.stage_ev[slot]));
+        par_memcpy((char*)dst_host + off, (const char*)h.stage_host + (size_t)slot * kStagePiece,
+                   nb);
+        ++drained;
+        if (issued < npieces) issue(issued++);
+    }
+}
+}  // namespace cf
 
 // ============================================================================
 // C-ABI
@@ -1705,14 +1785,12 @@ extern "C" int cf_solve_rows(void* hp, const double* rows, int64_t count,
         int kc = pick_kc(count - done);
         int cnt = (int)std::min<int64_t>(kc, count - done);
         h.ensure_workspace(kc);
-        CF_CUDA(cudaMemcpyAsync(h.S, rows + done * n, sizeof(double) * cnt * n,
-                                cudaMemcpyHostToDevice, h.s));
+        h2d_staged(h, h.S, rows + done * n, sizeof(double) * cnt * n);
         rows_to_block(h, h.S, cnt, kc, h.B);
         std::vector<double> res(kc, 0.0);
         solve_block(h, kc, cnt, *p, res.data(), *st);
         block_to_rows(h, h.X, cnt, kc, h.S);
-        CF_CUDA(cudaMemcpyAsync(out_rows + done * n, h.S, sizeof(double) * cnt * n,
-                                cudaMemcpyDeviceToHost, h.s));
+        d2h_staged(h, out_rows + done * n, h.S, sizeof(double) * cnt * n);
         CF_CUDA(cudaStreamSynchronize(h.s));
         std::memcpy(residuals + done, res.data(), sizeof(double) * cnt);
         done += cnt;
