@@ -161,6 +161,7 @@ def cpu_reference(cfgname: str, columns: int, budget_s: float, threads: int):
             break
     per = float(np.mean(times))
     return {"value": cols / per, "unit": "solves/s", "cores": nthreads, "kind": "port",
+            "workload": f"{bc.name.upper()}: {bc.description}", "n": g.n, "m": g.m,
             "sample": f"{cols} of {bc.jl_k} {cfgname.upper()} JL right-hand sides "
                       f"(tau {bc.tau:g}), {len(blocks)} x 64-column blocks, "
                       f"{len(times)} timed repetition(s); oracle port of pkg/src/cfcent",
@@ -177,7 +178,8 @@ def run_reference_arm(args):
             "steps": r["steps_timed"], "warmup": 0, "ms_per_step": r["s_per_step"] * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, SURVEY.md §8(d) recipes)", "impl": "reference",
-            "config": {"workload": args.config.upper(), "rhs_per_step": args.ref_columns},
+            "config": {"workload": r["workload"], "n": r["n"], "m": r["m"],
+                       "rhs_per_step": args.ref_columns},
             "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": r["value"], "unit": "solves/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
@@ -316,6 +318,24 @@ def run_gpu_arm(args):
     h2d = rhs.nbytes
     d2h = rhs.nbytes + 8 * rhs.shape[0]
 
+    # sampling estimator (configs that name one): pivots + query solved in one batch
+    sampling = None
+    if bc.sampling_pivots and world == 1:
+        P.cf_closeness_sampling(g, h, bc.sampling_query, bc.sampling_pivots, bc.sampling_seed, cfg)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        tab = P.cf_closeness_sampling(g, h, bc.sampling_query, bc.sampling_pivots,
+                                      bc.sampling_seed, cfg)
+        b.record(stream)
+        torch.cuda.synchronize()
+        sms = a.elapsed_time(b)
+        nsolve = len(set(P.pivot_set(g.n, bc.sampling_pivots, bc.sampling_seed).tolist())
+                     | set(bc.sampling_query))
+        sampling = {"pivots": bc.sampling_pivots, "rhs": nsolve, "seconds_per_estimate": sms / 1e3,
+                    "solves_per_s": nsolve / (sms / 1e3),
+                    "score_first_query": float(tab.vector(bc.sampling_query[:1])[0])}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_reference(args.config, args.cpu_columns, args.cpu_budget, 1)
@@ -338,6 +358,7 @@ def run_gpu_arm(args):
                          "ms_per_launch": dom_ms_per_launch},
             "step_hbm_gbs": total_bytes / (prof_ms * 1e-3) / 1e9 if prof_ms > 0 else None,
             "cpu_baseline": cpu,
+            "sampling": sampling,
             "e2e": {"value": e2e_value, "unit": "solves/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "api": "solve_many (host supplies)"},
             "gpu_launches": launches * args.steps,

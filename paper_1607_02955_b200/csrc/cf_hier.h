@@ -53,6 +53,7 @@ struct DLevel {
     // per colour class (host, for the algorithmic-bytes model): rows, nnz,
     // distinct neighbour rows
     std::vector<int64_t> c_rows, c_nnz, c_nbr;
+    int64_t merged_nbr = 0;  // distinct neighbour rows of the merged Jacobi classes
     int64_t w_nnz = 0;  // elimination: nnz(W_cf)
     int gs_classes = 0;  // colour classes swept one by one (<= kGsClasses)
     bool merged = false; // classes >= kGsClasses merged into one Jacobi step

@@ -353,6 +353,136 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : kGatherCtas)) k_gs(
     stv<V>(X + i * KC + c0, acc);
 }
 
+// Row-pipelined smoother sweep over a contiguous row range [base, base + cnt)
+// (colour classes are contiguous in the device order).  Warp w owns rows
+// [w*kPipeRows, (w+1)*kPipeRows) of the range and, while the neighbour rows of
+// its current row are in flight, already loads the next row's row pointer,
+// first index/value chunk, b and diagonal, so a light row costs about one
+// dependent round trip.  Warps past the row warps take heavy-row segments
+// (SegWork) as in k_gs.  GS writes x in place; JACOBI writes T[q].
+constexpr int kPipeRows = 8;
+#ifndef CF_PIPE_CTAS
+#define CF_PIPE_CTAS 2
+#endif
+#ifndef CF_USE_PIPE
+#define CF_USE_PIPE 0
+#endif
+template <int KC, bool JACOBI>
+__global__ void __launch_bounds__(kThreads, CF_PIPE_CTAS)
+    k_sweep_pipe(int base, int cnt, int64_t nrw, int64_t nnz_total,
+                 const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                 const double* __restrict__ val, const double* __restrict__ diag,
+                 const double* __restrict__ B, double* __restrict__ X, double* __restrict__ T,
+                 int from_zero, HeavyDev H, SegWork w) {
+    CF_LANE_SETUP(KC)
+    constexpr int W = Lt::LPR;
+    constexpr unsigned MASK = W == 32 ? 0xffffffffu : ((1u << W) - 1u);
+    constexpr int G0 = CF_GATHER_DOUBLES / V;
+    constexpr int G = W < G0 ? W : G0;
+    const int64_t gw = (int64_t)blockIdx.x * Lt::RPB + slot;
+    if (!lane_ok) return;
+    if (gw >= nrw) {  // heavy-row segment warp
+        int64_t sg = w.s_lo + (gw - nrw);
+        if (sg >= w.s_hi) return;
+        DV<V> acc;
+        int hv;
+        if (!seg_item<KC>(w, sg, col, val, X, c0, hv, acc)) return;
+        const int64_t i = w.h_row[hv];
+        DV<V> b = ldv<V>(B + i * KC + c0);
+        const double d = diag[i];
+#pragma unroll
+        for (int t = 0; t < V; ++t) acc.v[t] = (b.v[t] - acc.v[t]) / d;
+        if constexpr (JACOBI)
+            stv<V>(T + (int64_t)(w.h_pos[hv] - base) * KC + c0, acc);
+        else
+            stv<V>(X + i * KC + c0, acc);
+        return;
+    }
+    const int64_t q0 = gw * kPipeRows, q1 = min((int64_t)cnt, q0 + kPipeRows);
+    if (q0 >= q1) return;
+    auto fetch = [&](int64_t p0, int& jj, double& aa) {
+        jj = 0;
+        aa = 0.0;
+        if (p0 + lane < nnz_total) {
+            jj = __ldg(col + p0 + lane);
+            aa = __ldg(val + p0 + lane);
+        }
+    };
+    int64_t i = base + q0;
+    int64_t b0 = rp[i], b1 = rp[i + 1];
+    int jj;
+    double aa;
+    fetch(b0, jj, aa);
+    DV<V> bv = ldv<V>(B + i * KC + c0);
+    double dv = diag[i];
+    for (int64_t q = q0; q < q1; ++q) {
+        i = base + q;
+        const bool has_next = q + 1 < q1;
+        // next row: metadata loads issued before this row's gathers
+        int64_t nb1 = 0;
+        int jn = 0;
+        double an = 0.0, dn = 1.0;
+        DV<V> bn;
+        zero(bn);
+        if (has_next) {
+            nb1 = rp[i + 2];
+            fetch(b1, jn, an);
+            bn = ldv<V>(B + (i + 1) * KC + c0);
+            dn = diag[i + 1];
+        }
+        const int64_t deg = b1 - b0;
+        DV<V> acc;
+        zero(acc);
+        bool write = true;
+        if (from_zero) {
+            // x = b / d (all neighbours are still zero)
+        } else if (H.hv && deg > kHeavyNnz) {
+            write = false;  // finished by its last segment warp
+        } else {
+            int64_t p0 = b0;
+            int cj = jj;
+            double ca = aa;
+            while (p0 < b1) {
+                const int cnt_c = (int)min((int64_t)W, b1 - p0);
+                for (int u0 = 0; u0 < cnt_c; u0 += G) {
+                    DV<V> x[G];
+                    double a[G];
+#pragma unroll
+                    for (int u = 0; u < G; ++u) {
+                        int j = __shfl_sync(MASK, cj, u0 + u, W);
+                        a[u] = __shfl_sync(MASK, ca, u0 + u, W);
+                        if (u0 + u < cnt_c)
+                            x[u] = ldv<V>(X + (size_t)j * KC + c0);
+                        else
+                            zero(x[u]);
+                    }
+#pragma unroll
+                    for (int u = 0; u < G; ++u)
+                        if (u0 + u < cnt_c)
+#pragma unroll
+                            for (int t = 0; t < V; ++t) acc.v[t] = fma(a[u], x[u].v[t], acc.v[t]);
+                }
+                p0 += W;
+                if (p0 < b1) fetch(p0, cj, ca);
+            }
+        }
+        if (write) {
+#pragma unroll
+            for (int t = 0; t < V; ++t) acc.v[t] = (bv.v[t] - acc.v[t]) / dv;
+            if constexpr (JACOBI)
+                stv<V>(T + q * KC + c0, acc);
+            else
+                stv<V>(X + i * KC + c0, acc);
+        }
+        b0 = b1;
+        b1 = nb1;
+        jj = jn;
+        aa = an;
+        bv = bn;
+        dv = dn;
+    }
+}
+
 // Merged trailing colour classes, one Jacobi step: T[q] = (b_i - sum_j L_ij x_j) / L_ii
 // for i = rows[q] with every x_j read before any row of the step is written
 // (k_scatter_rows then writes T back).  Heavy rows as in k_gs.
@@ -915,6 +1045,13 @@ struct Ops {
         ProfScope ps(h, "gs_sweep", lev,
                      12.0 * l.c_nnz[colr] + 20.0 * cnt +
                          Vb(2 * cnt + (from_zero ? 0 : l.c_nbr[colr])));
+        if (CF_USE_PIPE && l.contig) {
+            const int64_t nrw = (cnt + kPipeRows - 1) / kPipeRows;
+            k_sweep_pipe<KC, false><<<grid_rows<KC>(nrw + (w.s_hi - w.s_lo)), kThreads, 0, h.s>>>(
+                beg, cnt, nrw, l.nnz, l.rp, l.col, l.val, l.diag, b, x, nullptr,
+                from_zero ? 1 : 0, hd(h, l.pm), w);
+            return;
+        }
         k_gs<KC><<<grid_rows<KC>(cnt + (w.s_hi - w.s_lo)), kThreads, 0, h.s>>>(
             l.contig ? nullptr : l.crows + beg, beg, cnt, l.rp, l.col, l.val, l.diag, b, x,
             from_zero ? 1 : 0, hd(h, l.pm), w);
@@ -926,13 +1063,16 @@ struct Ops {
         if (cnt <= 0) return;
         const int lev = (int)(&l - &h.L[0]);
         SegWork w = segwork(h, l.pm, l.pm.cseg[K], l.pm.cseg[l.ncolors]);
-        int64_t nnz = 0, nbr = 0;
-        for (int c = K; c < l.ncolors; ++c) {
-            nnz += l.c_nnz[c];
-            nbr += l.c_nbr[c];
-        }
+        int64_t nnz = 0, nbr = l.merged_nbr;
+        for (int c = K; c < l.ncolors; ++c) nnz += l.c_nnz[c];
         {
             ProfScope ps(h, "jacobi_merged", lev, 12.0 * nnz + 20.0 * cnt + Vb(2 * cnt + nbr));
+            if (CF_USE_PIPE && l.contig) {
+                const int64_t nrw = (cnt + kPipeRows - 1) / kPipeRows;
+                k_sweep_pipe<KC, true><<<grid_rows<KC>(nrw + (w.s_hi - w.s_lo)), kThreads, 0,
+                                         h.s>>>(beg, cnt, nrw, l.nnz, l.rp, l.col, l.val, l.diag,
+                                                b, x, h.T, 0, hd(h, l.pm), w);
+            } else
             k_jacobi_rows<KC><<<grid_rows<KC>(cnt + (w.s_hi - w.s_lo)), kThreads, 0, h.s>>>(
                 l.contig ? nullptr : l.crows + beg, beg, cnt, l.rp, l.col, l.val, l.diag, b, x,
                 h.T, hd(h, l.pm), w);
@@ -1718,6 +1858,19 @@ extern "C" int cf_hier_create(int32_t nlev, const CfLevelDesc* ds, int32_t devic
                     l.c_rows.push_back(rows);
                     l.c_nnz.push_back(nnz);
                     l.c_nbr.push_back(nbr);
+                }
+                // distinct neighbour rows of the merged (Jacobi) classes, counted once
+                if (d.n_colors > kGsClasses) {
+                    std::vector<uint8_t> seen(d.n, 0);
+                    for (int32_t q = d.color_ptr[kGsClasses]; q < d.color_ptr[d.n_colors]; ++q) {
+                        int32_t i = d.color_rows[q];
+                        for (int64_t p = d.rowptr[i]; p < d.rowptr[i + 1]; ++p) {
+                            if (!seen[d.col[p]]) {
+                                seen[d.col[p]] = 1;
+                                ++l.merged_nbr;
+                            }
+                        }
+                    }
                 }
             } else if (d.kind == CF_LEVEL_ELIMINATION) {
                 l.nf = d.n_f;

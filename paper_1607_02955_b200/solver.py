@@ -74,6 +74,8 @@ DEVICE_REORDER = True
 # every level when n0 > STALL_BREAKER_MIN_N0; graphs whose hierarchies never
 # stall there (C1-C3) keep the reference hierarchy exactly.
 STALL_ELIM_CAP = 16
+STALL_ELIM_CAPS = (16, 64, 256, 1024)   # escalation, each under the fill budget
+STALL_FILL_FACTOR = 2.0                 # min(sum d_f^2, |C|^2) <= factor * nnz
 STALL_AGG_CAP = 64
 STALL_AGG_THRESHOLD = 0.0
 STALL_BREAKER_MIN_N0 = 262144
@@ -465,7 +467,23 @@ def coarsen_eliminate(matrix: sp.csr_matrix, degree_cap: int = 4):
                                          N.ptr(out, N.i64p), N.ptr(cnt, N.i64p)))
     if cnt[0] == 0:
         return matrix, None
-    f = out[:cnt[0]].copy()
+    return _eliminate_set(matrix, out[:cnt[0]].copy())
+
+
+def _elim_select(matrix: sp.csr_matrix, cap: int) -> np.ndarray:
+    """Greedy ascending-id independent set of off-degree <= cap (native)."""
+    n = matrix.shape[0]
+    ip, ix = _csr64(matrix)
+    out = np.empty(max(n, 1), dtype=np.int64)
+    cnt = np.zeros(1, dtype=np.int64)
+    N.check(N.lib().cf_setup_elim_select(n, N.ptr(ip, N.i64p), N.ptr(ix, N.i64p), int(cap),
+                                         N.ptr(out, N.i64p), N.ptr(cnt, N.i64p)))
+    return out[:cnt[0]].copy()
+
+
+def _eliminate_set(matrix: sp.csr_matrix, f: np.ndarray):
+    """Exact Schur complement of the independent set f (solver.py:251-261)."""
+    n = matrix.shape[0]
     in_f = np.zeros(n, dtype=bool)
     in_f[f] = True
     c = np.flatnonzero(~in_f)
@@ -625,7 +643,24 @@ def setup(matrix: sp.spmatrix, config: SolverConfig | None = None,
         applied = next((k for k in (preferred, other) if stage(k)[0] >= need), None)
         if applied is None and breaker_on(n_cur):
             stage(LevelKind.AGGREGATION)
-            schur, rec = coarsen_eliminate(current, STALL_ELIM_CAP)
+            offdeg = np.diff(current.indptr) - 1
+            best_f = None
+            for ecap in STALL_ELIM_CAPS:
+                f = _elim_select(current, ecap)
+                if f.size == n_cur and n_cur > 0:
+                    f = f[:-1]
+                # Schur fill is at most sum d_f^2 entries, and never more than the
+                # remaining |C|^2 positions (duplicates merge)
+                fill = min(float(np.sum(offdeg[f].astype(np.float64) ** 2)),
+                           float(n_cur - f.size) ** 2)
+                if fill > STALL_FILL_FACTOR * current.nnz and best_f is not None:
+                    break
+                if best_f is None or f.size > best_f.size:
+                    best_f = f
+            if best_f is not None and best_f.size:
+                schur, rec = _eliminate_set(current, best_f)
+            else:
+                schur, rec = current, None
             alt = {"elim": (0 if rec is None else rec.f_nodes.size, schur, rec)}
             co, ag = coarsen_aggregate(current, tvecs[n_cur], STALL_AGG_CAP, STALL_AGG_THRESHOLD)
             alt["agg"] = (n_cur - (int(ag.max()) + 1), co, ag)

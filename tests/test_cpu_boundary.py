@@ -143,3 +143,46 @@ def test_generators_match_oracle():
     g = G.barabasi_albert_graph(3000, 4, 1)
     og = O.barabasi_albert(3000, 4, 1)
     assert np.array_equal(g.indptr, og[0]) and np.array_equal(g.indices, og[1])
+
+
+def test_stall_breaker_on_bipartite_core():
+    """K_{40,6000}-like core: the reference rule shrinks it by ~40 nodes per
+    level; the stall breaker eliminates the leaf side at once (exact Schur)."""
+    rng = np.random.default_rng(3)
+    hubs, leaves = 40, 6000
+    u, v = [], []
+    for leaf in range(leaves):
+        for hb in rng.choice(hubs, size=20, replace=False):
+            u.append(int(hb))
+            v.append(hubs + leaf)
+    g = P.Graph.from_edges(u, v, n=hubs + leaves)
+    ref = P.setup(P.laplacian(g), P.SolverConfig(), stall_breaker=False)
+    new = P.setup(P.laplacian(g), P.SolverConfig(), stall_breaker=True)
+    assert len(new.levels) <= 3 < len(ref.levels)
+    assert new.levels[0].kind is LevelKind.ELIMINATION and new.levels[0].f_nodes.size >= leaves - 1
+    sizes = new.level_sizes
+    assert all(a > b for a, b in zip(sizes, sizes[1:])) and sizes[-1] <= 200
+    # default (auto) keeps the reference hierarchy on small graphs below 4096 nodes
+    small = P.setup(P.laplacian(G.grid_graph(40)))
+    assert small.level_sizes == P.setup(P.laplacian(G.grid_graph(40)),
+                                        stall_breaker=False).level_sizes
+
+
+def test_device_level_views_are_same_operator(rng):
+    """The truncated + RCM/colour-reordered device hierarchy describes the same
+    operators as the host hierarchy (checked on host)."""
+    from paper_1607_02955_b200.solver import device_levels, permute_levels
+    g = G.barabasi_albert_graph(20000, 4, 3)
+    h = P.setup(P.laplacian(g))
+    dl = device_levels(h.levels)
+    assert dl[-1].kind is LevelKind.COARSEST and dl[-1].size <= max(4096, 200)
+    pl, perm0 = permute_levels(dl)
+    A0 = h.levels[0].matrix
+    assert abs(pl[0].matrix - A0[perm0][:, perm0]).max() < 1e-14
+    for lvl in pl:
+        if lvl.kind is LevelKind.AGGREGATION:
+            A = lvl.matrix
+            rows = np.repeat(np.arange(A.shape[0]), np.diff(A.indptr))
+            off = A.indices != rows
+            assert not np.any(lvl.colors[rows[off]] == lvl.colors[A.indices[off]])
+            assert np.all(np.diff(lvl.colors) >= 0)  # classes contiguous
