@@ -190,6 +190,11 @@ int cf_setup_aggregate(int64_t n, const int64_t* indptr, const int64_t* indices,
 /* solver.py:364-380: greedy matching over a pre-sorted edge order. */
 int cf_setup_matching(int64_t n, int64_t n_edges, const int64_t* eu, const int64_t* ev,
                       const int64_t* order, int64_t* out_agg, int64_t* n_agg);
+/* graph.py:100-147 Graph.from_edges core: symmetric CSR of m (loop-free,
+ * in-range) edges, neighbours sorted, duplicates summed in input order.
+ * indptr: n+1; indices/weights: room for 2m entries; *nnz = entries written. */
+int cf_build_csr(int64_t n, int64_t m, const int64_t* u, const int64_t* v, const double* w,
+                 int64_t* indptr, int64_t* indices, double* weights, int64_t* nnz);
 /* greedy natural-order colouring of the off-diagonal graph (multicolour
  * Gauss-Seidel, the B200 smoother ordering). */
 int cf_setup_colour(int64_t n, const int64_t* indptr, const int64_t* indices,

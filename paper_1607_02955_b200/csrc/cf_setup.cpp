@@ -158,3 +158,54 @@ extern "C" int cf_setup_colour(int64_t n, const int64_t* indptr, const int64_t* 
     *n_colors = nc;
     return CF_OK;
 }
+
+extern "C" int cf_build_csr(int64_t n, int64_t m, const int64_t* u, const int64_t* v,
+                            const double* w, int64_t* indptr, int64_t* indices, double* weights,
+                            int64_t* nnz_out) {
+    // graph.py:133-146: entries (u,v,w) then (v,u,w) in input order, stable
+    // sort by (row, col), duplicates summed left to right.  Counting sort by
+    // row keeps input order; a stable per-row sort by column follows.
+    CF_API_BEGIN
+    std::vector<int64_t> cnt(n + 1, 0);
+    for (int64_t e = 0; e < m; ++e) {
+        ++cnt[u[e] + 1];
+        ++cnt[v[e] + 1];
+    }
+    for (int64_t i = 0; i < n; ++i) cnt[i + 1] += cnt[i];
+    std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
+    std::vector<int64_t> col(2 * m);
+    std::vector<double> val(2 * m);
+    for (int64_t e = 0; e < m; ++e) {  // first all (u -> v) entries, then all (v -> u)
+        int64_t p = pos[u[e]]++;
+        col[p] = v[e];
+        val[p] = w[e];
+    }
+    for (int64_t e = 0; e < m; ++e) {
+        int64_t p = pos[v[e]]++;
+        col[p] = u[e];
+        val[p] = w[e];
+    }
+    int64_t out = 0;
+    indptr[0] = 0;
+    std::vector<int64_t> ord;
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t a = cnt[i], b = cnt[i + 1];
+        ord.resize(b - a);
+        for (int64_t q = 0; q < b - a; ++q) ord[q] = a + q;
+        std::stable_sort(ord.begin(), ord.end(),
+                         [&](int64_t x, int64_t y) { return col[x] < col[y]; });
+        for (size_t q = 0; q < ord.size();) {
+            int64_t c = col[ord[q]];
+            double s = val[ord[q]];
+            size_t r = q + 1;
+            while (r < ord.size() && col[ord[r]] == c) s += val[ord[r++]];
+            indices[out] = c;
+            weights[out] = s;
+            ++out;
+            q = r;
+        }
+        indptr[i + 1] = out;
+    }
+    *nnz_out = out;
+    CF_API_END
+}

@@ -100,20 +100,38 @@ class Graph:
             n = int(max(u.max(initial=-1), v.max(initial=-1)) + 1)
         if u.size and (min(u.min(), v.min()) < 0 or max(u.max(), v.max()) >= n):
             raise DomainError("node ids out of range")
-        src = np.concatenate([u, v])
-        dst = np.concatenate([v, u])
-        wt = np.concatenate([w, w])
-        order = np.lexsort((dst, src))
-        src, dst, wt = src[order], dst[order], wt[order]
-        if src.size:
+        # symmetrise, sort neighbours, merge duplicates (graph.py:133-146):
+        # native counting sort (csrc/cf_setup.cpp) when no edge repeats
+        from . import _native as N
+
+        u = np.ascontiguousarray(u, dtype=np.int64)
+        v = np.ascontiguousarray(v, dtype=np.int64)
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        indptr = np.empty(n + 1, dtype=np.int64)
+        dst = np.empty(2 * u.size, dtype=np.int64)
+        wt = np.empty(2 * u.size, dtype=np.float64)
+        nnz = np.zeros(1, dtype=np.int64)
+        N.check(N.lib().cf_build_csr(n, u.size, N.ptr(u, N.i64p), N.ptr(v, N.i64p),
+                                     N.ptr(w, N.f64p), N.ptr(indptr, N.i64p), N.ptr(dst, N.i64p),
+                                     N.ptr(wt, N.f64p), N.ptr(nnz, N.i64p)))
+        if nnz[0] == 2 * u.size:
+            dst, wt = dst[:nnz[0]], wt[:nnz[0]]
+        else:
+            # duplicates were merged: redo with numpy's own reduction so the
+            # summed weights match the reference bit-for-bit on this machine
+            src = np.concatenate([u, v])
+            dst = np.concatenate([v, u])
+            wt = np.concatenate([w, w])
+            order = np.lexsort((dst, src))
+            src, dst, wt = src[order], dst[order], wt[order]
             first = np.empty(src.size, dtype=bool)
             first[0] = True
             np.logical_or(src[1:] != src[:-1], dst[1:] != dst[:-1], out=first[1:])
             starts = np.flatnonzero(first)
             wt = np.add.reduceat(wt, starts)
             src, dst = src[starts], dst[starts]
-        indptr = np.zeros(n + 1, dtype=np.int64)
-        np.cumsum(np.bincount(src, minlength=n), out=indptr[1:])
+            indptr = np.zeros(n + 1, dtype=np.int64)
+            np.cumsum(np.bincount(src, minlength=n), out=indptr[1:])
         return Graph(indptr=indptr, indices=dst, weights=wt, node_labels=node_labels)
 
 
