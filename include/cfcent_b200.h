@@ -190,6 +190,11 @@ int cf_setup_aggregate(int64_t n, const int64_t* indptr, const int64_t* indices,
 /* solver.py:364-380: greedy matching over a pre-sorted edge order. */
 int cf_setup_matching(int64_t n, int64_t n_edges, const int64_t* eu, const int64_t* ev,
                       const int64_t* order, int64_t* out_agg, int64_t* n_agg);
+/* solver.py:167-187 _rebuild_laplacian on a CSR without duplicates:
+ * out capacity 2*nnz + n entries; *nnz = entries written (sorted rows). */
+int cf_rebuild_laplacian(int64_t n, const int64_t* indptr, const int64_t* indices,
+                         const double* data, int64_t* out_ptr, int64_t* out_idx,
+                         double* out_val, int64_t* nnz);
 /* graph.py:100-147 Graph.from_edges core: symmetric CSR of m (loop-free,
  * in-range) edges, neighbours sorted, duplicates summed in input order.
  * indptr: n+1; indices/weights: room for 2m entries; *nnz = entries written. */

@@ -94,6 +94,7 @@ struct Hier {
     size_t parts_cap = 0;  // doubles
     double* SP = nullptr;  // heavy-row segment partials, max_nseg x kc_ws
     double* fin = nullptr; // finalize stage-1 scratch
+    double* DP = nullptr;  // dense coarse apply: per-chunk partials
     double* T = nullptr;   // merged-class Jacobi staging, max_merged x kc_ws
     int64_t max_merged = 0;
     int64_t max_nseg = 0;

@@ -209,3 +209,77 @@ extern "C" int cf_build_csr(int64_t n, int64_t m, const int64_t* u, const int64_
     *nnz_out = out;
     CF_API_END
 }
+
+extern "C" int cf_rebuild_laplacian(int64_t n, const int64_t* indptr, const int64_t* indices,
+                                    const double* data, int64_t* out_ptr, int64_t* out_idx,
+                                    double* out_val, int64_t* nnz_out) {
+    // solver.py:167-187 _rebuild_laplacian: (M + M^T) * 0.5, keep strictly
+    // negative off-diagonals, diagonal = 0 - v_1 - v_2 - ... over the kept
+    // off-diagonals of the row in column order (np.add.at order), sorted
+    // indices.  Input: CSR without duplicate entries (any column order).
+    CF_API_BEGIN
+    const int64_t nnz = indptr[n];
+    // transpose by counting sort
+    std::vector<int64_t> tptr(n + 1, 0);
+    for (int64_t p = 0; p < nnz; ++p) ++tptr[indices[p] + 1];
+    for (int64_t i = 0; i < n; ++i) tptr[i + 1] += tptr[i];
+    std::vector<int64_t> tpos(tptr.begin(), tptr.end() - 1), tidx(nnz);
+    std::vector<double> tval(nnz);
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) {
+            int64_t q = tpos[indices[p]]++;
+            tidx[q] = i;
+            tval[q] = data[p];
+        }
+    std::vector<double> acc(n, 0.0);
+    std::vector<int64_t> mark(n, -1), cols;
+    int64_t out = 0;
+    out_ptr[0] = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        cols.clear();
+        for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) {
+            int64_t j = indices[p];
+            if (mark[j] != i) {
+                mark[j] = i;
+                acc[j] = 0.0;
+                cols.push_back(j);
+            }
+            acc[j] += data[p];
+        }
+        for (int64_t p = tptr[i]; p < tptr[i + 1]; ++p) {
+            int64_t j = tidx[p];
+            if (mark[j] != i) {
+                mark[j] = i;
+                acc[j] = 0.0;
+                cols.push_back(j);
+            }
+            acc[j] += tval[p];
+        }
+        std::sort(cols.begin(), cols.end());
+        double dg = 0.0;
+        for (int64_t j : cols) {
+            double v = acc[j] * 0.5;
+            if (j != i && v < 0.0) dg += -v;
+        }
+        bool placed = false;
+        for (int64_t j : cols) {
+            if (!placed && j > i) {
+                out_idx[out] = i;
+                out_val[out++] = dg;
+                placed = true;
+            }
+            double v = acc[j] * 0.5;
+            if (j != i && v < 0.0) {
+                out_idx[out] = j;
+                out_val[out++] = v;
+            }
+        }
+        if (!placed) {
+            out_idx[out] = i;
+            out_val[out++] = dg;
+        }
+        out_ptr[i + 1] = out;
+    }
+    *nnz_out = out;
+    CF_API_END
+}

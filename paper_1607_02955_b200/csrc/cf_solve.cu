@@ -693,107 +693,99 @@ __global__ void __launch_bounds__(kThreads, 2) k_elim_interp(
 }
 
 // coarsest: x = M b, M dense n x n (solver.py:406-419 restated as one operator).
-// Register-tiled fp64 GEMM: a CTA computes 32 rows x KC columns; every output
-// is one fma chain over l ascending (width-independent, deterministic).
-constexpr int kDenseTR = 32, kDenseTL = 16;
+// The l range is cut into dense_splits(n) fixed chunks; every output is, per
+// chunk, one fma chain over l ascending, and the chunk partials are summed in
+// chunk order (k_dense_reduce) -- the same order for every block width.
+// split count fills one wave of 148 SMs with the 128-row tiles (1 CTA/SM by
+// registers); a function of n only, so every block width sums in one order
+static inline int dense_splits(int n) {
+    const int row_tiles = (n + 127) / 128;
+    return n <= 256 ? 1 : std::max(1, std::min(16, 148 / row_tiles));
+}
+static inline int dense_chunk(int n, int S) { return (((n + S - 1) / S) + 15) / 16 * 16; }
+
+// small widths: one thread per (row, column) output, per chunk
 template <int KC>
-__global__ void __launch_bounds__(kThreads) k_dense(int n, const double* __restrict__ M,
-                                                    const double* __restrict__ B,
-                                                    double* __restrict__ X) {
-    constexpr int CG = KC >= 16 ? 16 : KC;             // column groups
-    constexpr int RG = kThreads / CG;                   // row groups
-    constexpr int RPT = (kDenseTR + RG - 1) / RG;       // rows per thread
-    constexpr int CPT = KC / CG;                        // columns per thread
-    __shared__ double sA[kDenseTL][kDenseTR + 1];
-    __shared__ double sB[kDenseTL][KC];
-    const int tid = threadIdx.x, tc = tid % CG, tr = tid / CG;
-    const int i0 = blockIdx.x * kDenseTR;
-    double acc[RPT][CPT];
+__global__ void __launch_bounds__(kThreads) k_dense_small(int n, int chunk,
+                                                          const double* __restrict__ M,
+                                                          const double* __restrict__ B,
+                                                          double* __restrict__ P) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int s = blockIdx.y;
+    if (t >= (int64_t)n * KC) return;
+    const int64_t i = t / KC;
+    const int c = (int)(t % KC);
+    const int l0 = s * chunk, l1 = min(n, l0 + chunk);
+    double acc = 0.0;
+    for (int l = l0; l < l1; ++l) acc = fma(__ldg(M + i * n + l), __ldg(B + (size_t)l * KC + c), acc);
+    P[((size_t)s * n + i) * KC + c] = acc;
+}
+
+// wide blocks: 128 x TC output tile per CTA (TC = min(KC,128)), 16-deep l
+// stages in shared memory, 8 x (TC/16) register tile per thread.
+constexpr int kGR = 128, kGL = 16;
+template <int KC>
+__global__ void __launch_bounds__(kThreads) k_dense_tile(int n, int chunk,
+                                                         const double* __restrict__ M,
+                                                         const double* __restrict__ B,
+                                                         double* __restrict__ P) {
+    constexpr int TC = KC < 128 ? KC : 128;
+    constexpr int CT = TC / 16;
+    __shared__ double sA[kGL][kGR + 2];
+    __shared__ double sB[kGL][TC];
+    const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+    const int i0 = blockIdx.x * kGR, j0 = blockIdx.y * TC, s = blockIdx.z;
+    const int l0 = s * chunk, l1 = min(n, l0 + chunk);
+    double acc[8][CT];
 #pragma unroll
-    for (int r = 0; r < RPT; ++r)
+    for (int r = 0; r < 8; ++r)
 #pragma unroll
-        for (int c = 0; c < CPT; ++c) acc[r][c] = 0.0;
-    for (int l0 = 0; l0 < n; l0 += kDenseTL) {
-        for (int e = tid; e < kDenseTR * kDenseTL; e += kThreads) {
-            int r = e / kDenseTL, t = e % kDenseTL;
-            sA[t][r] = (i0 + r < n && l0 + t < n) ? M[(size_t)(i0 + r) * n + l0 + t] : 0.0;
+        for (int c = 0; c < CT; ++c) acc[r][c] = 0.0;
+    for (int lb = l0; lb < l1; lb += kGL) {
+        for (int e = tid; e < kGR * kGL; e += kThreads) {
+            const int r = e / kGL, t = e % kGL;
+            const int i = i0 + r, l = lb + t;
+            sA[t][r] = (i < n && l < l1) ? __ldg(M + (size_t)i * n + l) : 0.0;
         }
-        for (int e = tid; e < kDenseTL * KC; e += kThreads) {
-            int t = e / KC, c = e % KC;
-            sB[t][c] = (l0 + t < n) ? B[(size_t)(l0 + t) * KC + c] : 0.0;
+        for (int e = tid; e < kGL * TC; e += kThreads) {
+            const int t = e / TC, c = e % TC;
+            const int l = lb + t;
+            sB[t][c] = (l < l1) ? __ldg(B + (size_t)l * KC + j0 + c) : 0.0;
         }
         __syncthreads();
-#pragma unroll 4
-        for (int t = 0; t < kDenseTL; ++t) {
-            double a[RPT], bb[CPT];
+        const int tmax = min(kGL, l1 - lb);
+        for (int t = 0; t < tmax; ++t) {
+            double a[8], bb[CT];
 #pragma unroll
-            for (int r = 0; r < RPT; ++r) {
-                int rr = tr + r * RG;
-                a[r] = rr < kDenseTR ? sA[t][rr] : 0.0;
-            }
+            for (int r = 0; r < 8; ++r) a[r] = sA[t][ty * 8 + r];
 #pragma unroll
-            for (int c = 0; c < CPT; ++c) bb[c] = sB[t][tc + c * CG];
+            for (int c = 0; c < CT; ++c) bb[c] = sB[t][tx + 16 * c];
 #pragma unroll
-            for (int r = 0; r < RPT; ++r)
+            for (int r = 0; r < 8; ++r)
 #pragma unroll
-                for (int c = 0; c < CPT; ++c) acc[r][c] = fma(a[r], bb[c], acc[r][c]);
+                for (int c = 0; c < CT; ++c) acc[r][c] = fma(a[r], bb[c], acc[r][c]);
         }
         __syncthreads();
     }
 #pragma unroll
-    for (int r = 0; r < RPT; ++r) {
-        int rr = tr + r * RG, i = i0 + rr;
-        if (rr < kDenseTR && i < n)
+    for (int r = 0; r < 8; ++r) {
+        const int i = i0 + ty * 8 + r;
+        if (i < n)
 #pragma unroll
-            for (int c = 0; c < CPT; ++c) X[(size_t)i * KC + tc + c * CG] = acc[r][c];
+            for (int c = 0; c < CT; ++c) P[((size_t)s * n + i) * KC + j0 + tx + 16 * c] = acc[r][c];
     }
 }
 
-// Wide blocks (KC >= 64): 64 x 64 output tiles (column-split grid), 4 x 4
-// register tile per thread, 32-deep l stages; same per-output fma order.
-constexpr int kDT = 64, kDL = 32;
+// X = sum over chunks of P[s] in chunk order
 template <int KC>
-__global__ void __launch_bounds__(kThreads) k_dense_wide(int n, const double* __restrict__ M,
-                                                         const double* __restrict__ B,
-                                                         double* __restrict__ X) {
-    __shared__ double sA[kDL][kDT + 2];
-    __shared__ double sB[kDL][kDT];
-    const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
-    const int i0 = blockIdx.x * kDT, j0 = blockIdx.y * kDT;
-    double acc[4][4];
-#pragma unroll
-    for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
-    for (int l0 = 0; l0 < n; l0 += kDL) {
-        for (int e = tid; e < kDT * kDL; e += kThreads) {
-            int r = e / kDL, t = e % kDL;
-            sA[t][r] = (i0 + r < n && l0 + t < n) ? M[(size_t)(i0 + r) * n + l0 + t] : 0.0;
-            int tb = e / kDT, cb = e % kDT;
-            sB[tb][cb] = (l0 + tb < n) ? B[(size_t)(l0 + tb) * KC + j0 + cb] : 0.0;
-        }
-        __syncthreads();
-#pragma unroll 8
-        for (int t = 0; t < kDL; ++t) {
-            double a[4], bb[4];
-#pragma unroll
-            for (int r = 0; r < 4; ++r) a[r] = sA[t][ty * 4 + r];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) bb[c] = sB[t][tx + 16 * c];
-#pragma unroll
-            for (int r = 0; r < 4; ++r)
-#pragma unroll
-                for (int c = 0; c < 4; ++c) acc[r][c] = fma(a[r], bb[c], acc[r][c]);
-        }
-        __syncthreads();
-    }
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        int i = i0 + ty * 4 + r;
-        if (i < n)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) X[(size_t)i * KC + j0 + tx + 16 * c] = acc[r][c];
-    }
+__global__ void __launch_bounds__(kThreads) k_dense_reduce(int n, int S,
+                                                           const double* __restrict__ P,
+                                                           double* __restrict__ X) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (int64_t)n * KC) return;
+    double acc = 0.0;
+    for (int s = 0; s < S; ++s) acc += P[(size_t)s * n * KC + t];
+    X[t] = acc;
 }
 
 // rows layout (cnt x n) -> block (n x KC), zero padding for columns >= cnt
@@ -971,13 +963,16 @@ struct Ops {
                 CF_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * (size_t)l.n * KC, h.s));
             } else {
                 ProfScope ps(h, "dense", j, 8.0 * l.n * l.n + 2 * Vb(l.n));
-                if constexpr (KC >= 64) {
-                    dim3 grd((unsigned)((l.n + kDT - 1) / kDT), KC / kDT);
-                    k_dense_wide<KC><<<grd, kThreads, 0, h.s>>>(l.n, l.M, b, x);
+                const int S = dense_splits(l.n), chunk = dense_chunk(l.n, S);
+                if constexpr (KC >= 16) {
+                    dim3 grd((unsigned)((l.n + kGR - 1) / kGR), KC / (KC < 128 ? KC : 128), S);
+                    k_dense_tile<KC><<<grd, kThreads, 0, h.s>>>(l.n, chunk, l.M, b, h.DP);
                 } else {
-                    k_dense<KC><<<(unsigned)((l.n + kDenseTR - 1) / kDenseTR), kThreads, 0,
-                                  h.s>>>(l.n, l.M, b, x);
+                    dim3 grd((unsigned)(((int64_t)l.n * KC + kThreads - 1) / kThreads), S);
+                    k_dense_small<KC><<<grd, kThreads, 0, h.s>>>(l.n, chunk, l.M, b, h.DP);
                 }
+                k_dense_reduce<KC><<<(unsigned)(((int64_t)l.n * KC + kThreads - 1) / kThreads),
+                                     kThreads, 0, h.s>>>(l.n, S, h.DP, x);
             }
             return;
         }
@@ -1566,6 +1561,7 @@ Hier::~Hier() {
     cudaFree(P);
     cudaFree(AP);
     cudaFree(parts);
+    cudaFree(DP);
     cudaFree(fin);
     cudaFree(SP);
     cudaFree(T);
@@ -1607,6 +1603,12 @@ void Hier::ensure_workspace(int kc) {
     re(SP, (size_t)std::max<int64_t>(max_nseg, 1) * kc);
     re(fin, (size_t)(3 * (np / kFinSeg + 2)) * kc);
     re(T, (size_t)std::max<int64_t>(max_merged, 1) * kc);
+    {
+        int64_t nd = 1;
+        for (auto& l : L)
+            if (l.kind == CF_LEVEL_COARSEST && l.M) nd = std::max<int64_t>(nd, (int64_t)dense_splits(l.n) * l.n);
+        re(DP, (size_t)nd * kc);
+    }
     if (Z) {
         cudaFree(Z); cudaFree(P); cudaFree(AP);
         Z = P = AP = nullptr;

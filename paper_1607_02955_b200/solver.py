@@ -401,9 +401,40 @@ class PotentialVector:
 # setup (host)
 # ---------------------------------------------------------------------------
 
-def _rebuild_laplacian(matrix: sp.spmatrix) -> sp.csr_matrix:
+def _rebuild_laplacian(matrix: sp.spmatrix, unique: bool = False) -> sp.csr_matrix:
     """Symmetrise; keep strictly negative off-diagonals; diagonal = minus the
-    off-diagonal row sum (solver.py:167-187)."""
+    off-diagonal row sum (solver.py:167-187).  Native (csrc/cf_setup.cpp) with
+    the reference's arithmetic; duplicate-carrying inputs take the scipy path."""
+    m = matrix.tocsr()
+    if unique or m.has_canonical_format or _no_duplicates(m):
+        n = m.shape[0]
+        ip = np.ascontiguousarray(m.indptr, dtype=np.int64)
+        ix = np.ascontiguousarray(m.indices, dtype=np.int64)
+        dv = np.ascontiguousarray(m.data, dtype=np.float64)
+        cap = 2 * ix.size + n
+        op = np.empty(n + 1, dtype=np.int64)
+        oi = np.empty(cap, dtype=np.int64)
+        ov = np.empty(cap, dtype=np.float64)
+        nnz = np.zeros(1, dtype=np.int64)
+        N.check(N.lib().cf_rebuild_laplacian(n, N.ptr(ip, N.i64p), N.ptr(ix, N.i64p),
+                                             N.ptr(dv, N.f64p), N.ptr(op, N.i64p),
+                                             N.ptr(oi, N.i64p), N.ptr(ov, N.f64p),
+                                             N.ptr(nnz, N.i64p)))
+        k = int(nnz[0])
+        out = sp.csr_matrix((ov[:k].copy(), oi[:k].astype(np.int32), op.astype(np.int32)),
+                            shape=(n, n))
+        out.has_sorted_indices = True
+        return out
+    return _rebuild_laplacian_scipy(m)
+
+
+def _no_duplicates(m: sp.csr_matrix) -> bool:
+    c = m.copy()
+    c.sum_duplicates()
+    return c.nnz == m.nnz
+
+
+def _rebuild_laplacian_scipy(matrix: sp.spmatrix) -> sp.csr_matrix:
     m = matrix.tocsr()
     m = (m + m.T) * 0.5
     t = m.tocoo()
@@ -490,7 +521,7 @@ def _eliminate_set(matrix: sp.csr_matrix, f: np.ndarray):
     d_f = matrix.diagonal()[f]
     w_cf = (-(matrix[c][:, f].tocsr())).tocsr()
     schur = matrix[c][:, c] - w_cf @ sp.diags(1.0 / d_f) @ w_cf.T
-    return _rebuild_laplacian(schur), EliminationRecord(f_nodes=f, c_nodes=c, f_degree=d_f,
+    return _rebuild_laplacian(schur, unique=True), EliminationRecord(f_nodes=f, c_nodes=c, f_degree=d_f,
                                                         w_cf=w_cf)
 
 
@@ -509,7 +540,7 @@ def relaxed_test_vectors(matrix: sp.csr_matrix, count: int, rng: np.random.Gener
 def _galerkin(matrix: sp.csr_matrix, agg: np.ndarray, n_agg: int) -> sp.csr_matrix:
     n = matrix.shape[0]
     p = sp.csr_matrix((np.ones(n), (np.arange(n), agg)), shape=(n, n_agg))
-    return _rebuild_laplacian(p.T @ matrix @ p)
+    return _rebuild_laplacian(p.T @ matrix @ p, unique=True)
 
 
 def coarsen_aggregate(matrix: sp.csr_matrix, test_vectors: np.ndarray,
