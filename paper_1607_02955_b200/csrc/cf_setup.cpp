@@ -231,18 +231,29 @@ extern "C" int cf_rebuild_laplacian(int64_t n, const int64_t* indptr, const int6
             tidx[q] = i;
             tval[q] = data[p];
         }
+    // scipy adds M + M^T with its canonical kernel (sorted output) when both
+    // operands have sorted, duplicate-free rows, else with the general kernel
+    // whose rows come out in reverse first-appearance order (M's row in
+    // storage order, then M^T's); the diagonal is accumulated in that order.
+    bool canonical = true;
+    for (int64_t i = 0; i < n && canonical; ++i)
+        for (int64_t p = indptr[i] + 1; p < indptr[i + 1]; ++p)
+            if (indices[p] <= indices[p - 1]) {
+                canonical = false;
+                break;
+            }
     std::vector<double> acc(n, 0.0);
-    std::vector<int64_t> mark(n, -1), cols;
+    std::vector<int64_t> mark(n, -1), cols, appear;
     int64_t out = 0;
     out_ptr[0] = 0;
     for (int64_t i = 0; i < n; ++i) {
-        cols.clear();
+        appear.clear();
         for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) {
             int64_t j = indices[p];
             if (mark[j] != i) {
                 mark[j] = i;
                 acc[j] = 0.0;
-                cols.push_back(j);
+                appear.push_back(j);
             }
             acc[j] += data[p];
         }
@@ -251,15 +262,24 @@ extern "C" int cf_rebuild_laplacian(int64_t n, const int64_t* indptr, const int6
             if (mark[j] != i) {
                 mark[j] = i;
                 acc[j] = 0.0;
-                cols.push_back(j);
+                appear.push_back(j);
             }
             acc[j] += tval[p];
         }
+        cols.assign(appear.begin(), appear.end());
         std::sort(cols.begin(), cols.end());
         double dg = 0.0;
-        for (int64_t j : cols) {
-            double v = acc[j] * 0.5;
-            if (j != i && v < 0.0) dg += -v;
+        if (canonical) {
+            for (int64_t j : cols) {
+                double v = acc[j] * 0.5;
+                if (j != i && v < 0.0) dg += -v;
+            }
+        } else {
+            for (auto it = appear.rbegin(); it != appear.rend(); ++it) {
+                int64_t j = *it;
+                double v = acc[j] * 0.5;
+                if (j != i && v < 0.0) dg += -v;
+            }
         }
         bool placed = false;
         for (int64_t j : cols) {

@@ -186,3 +186,44 @@ def test_device_level_views_are_same_operator(rng):
             off = A.indices != rows
             assert not np.any(lvl.colors[rows[off]] == lvl.colors[A.indices[off]])
             assert np.all(np.diff(lvl.colors) >= 0)  # classes contiguous
+
+
+def test_native_rebuild_matches_scipy_semantics(rng):
+    """cf_rebuild_laplacian reproduces solver.py:167-187 bit-for-bit, also for
+    unsorted (SpGEMM-output) rows where scipy's general binop order matters."""
+    import scipy.sparse as sp
+    from paper_1607_02955_b200 import solver as S
+    for t in range(12):
+        n = int(rng.integers(2, 200))
+        A = sp.random(n, n, density=0.05, random_state=int(rng.integers(1 << 30)), format="csr")
+        A.data = -A.data
+        A = (A + sp.diags(rng.uniform(0, 1, n))).tocsr()
+        if t % 2:
+            B = sp.random(n, n, density=0.04, random_state=int(rng.integers(1 << 30)), format="csr")
+            A = (A @ B @ B.T).tocsr()
+            A.data = -np.abs(A.data)
+            for i in range(n):
+                a, b = A.indptr[i], A.indptr[i + 1]
+                perm = rng.permutation(b - a)
+                A.indices[a:b] = A.indices[a:b][perm]
+                A.data[a:b] = A.data[a:b][perm]
+            A.has_sorted_indices = False
+        x = S._rebuild_laplacian(A, unique=True)
+        y = S._rebuild_laplacian_scipy(A)
+        assert np.array_equal(x.indptr, y.indptr) and np.array_equal(x.indices, y.indices)
+        assert np.array_equal(x.data, y.data)
+
+
+def test_native_csr_builder_matches_reference(rng):
+    from oracle import lamg_oracle as O
+    for t in range(6):
+        n = int(rng.integers(2, 500))
+        m = int(rng.integers(1, 3000))
+        u, v, w = rng.integers(0, n, m), rng.integers(0, n, m), rng.uniform(0.1, 3, m)
+        if t % 2:
+            k = np.unique(np.minimum(u, v) * n + np.maximum(u, v))
+            u, v, w = k // n, k % n, rng.uniform(0.1, 3, k.size)
+        g = P.Graph.from_edges(u, v, w, n=n)
+        ip, ix, ww = O.graph_from_edges(u, v, w, n=n)
+        assert np.array_equal(g.indptr, ip) and np.array_equal(g.indices, ix)
+        assert np.array_equal(g.weights, ww)

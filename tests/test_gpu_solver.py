@@ -158,3 +158,48 @@ def test_vs_oracle_bigger(rng):
     x = np.stack([p.values for p in P.solve_many(h, b)])
     ref, _ = O.solve_rows(oh, b)
     assert np.abs(x - ref).max() <= 1e-8 * np.abs(ref).max()
+
+
+@pytest.mark.slow
+def test_config3_properties():
+    """C3 (RGG 1e6): hierarchy equals the reference's recorded shape
+    (SURVEY.md A.2), every solve meets tau, JL sums additive over row ranges."""
+    import math
+    from paper_1607_02955_b200 import configs
+    from paper_1607_02955_b200.resistance import sketch_closeness_sums
+    bc = configs.make("c3")
+    assert (bc.graph.n, bc.graph.m) == (999896, 4995274)
+    cfg = P.SolverConfig(tau=bc.tau)
+    h = P.setup(P.laplacian(bc.graph), cfg)
+    assert h.level_sizes == [999896, 194376, 144154, 35917, 25678, 6364, 4862, 1165, 894, 209, 154]
+    eps = math.sqrt(math.log(bc.graph.n) / (bc.jl_k - 0.5))
+    k, full, res = sketch_closeness_sums(bc.graph, h, eps, 0, bc.query, cfg)
+    assert k == 128 and res.max() <= bc.tau
+    _, a, _ = sketch_closeness_sums(bc.graph, h, eps, 0, bc.query, cfg, rows=(0, 50))
+    _, b, _ = sketch_closeness_sums(bc.graph, h, eps, 0, bc.query, cfg, rows=(50, 128))
+    assert np.allclose(a + b, full, rtol=1e-10)
+    lap = P.laplacian(bc.graph)
+    rng = np.random.default_rng(3)
+    s = rng.standard_normal((3, bc.graph.n))
+    s -= s.mean(axis=1, keepdims=True)
+    for pot, b_ in zip(P.solve_many(h, s, cfg), s):
+        assert np.linalg.norm(b_ - lap @ pot.values) / np.linalg.norm(b_) <= bc.tau
+
+
+@pytest.mark.slow
+def test_config4_properties():
+    """C4 (R-MAT scale 20): generator reproduces the survey's LCC, the stall
+    breaker keeps the hierarchy shallow, solves meet tau."""
+    from paper_1607_02955_b200 import configs
+    bc = configs.make("c4")
+    assert (bc.graph.n, bc.graph.m) == (646140, 15700710)
+    cfg = P.SolverConfig(tau=bc.tau)
+    h = P.setup(P.laplacian(bc.graph), cfg)
+    assert len(h.levels) < 80
+    lap = P.laplacian(bc.graph)
+    rng = np.random.default_rng(4)
+    s = rng.standard_normal((9, bc.graph.n))
+    s -= s.mean(axis=1, keepdims=True)
+    for pot, b_ in zip(P.solve_many(h, s, cfg), s):
+        assert np.linalg.norm(b_ - lap @ pot.values) / np.linalg.norm(b_) <= bc.tau
+    assert h.stats.fallback_solves == 0
