@@ -108,6 +108,9 @@ struct Hier {
     std::vector<void*> owned;   // operator allocations
     int64_t bytes = 0;
     std::map<int, cudaGraphExec_t> cycle_graphs;  // per KC
+    std::map<int, cudaGraphExec_t> loop_graphs;   // whole outer iteration (while node)
+    int *d_iter = nullptr, *d_ncyc = nullptr;
+    long long* d_vcyc = nullptr;
     bool prof = false;
     std::vector<ProfRec> recs;
     std::vector<cudaEvent_t> ev_pool;

@@ -217,40 +217,65 @@ __global__ void __launch_bounds__(kThreads) k_fin2(const double* __restrict__ in
     }
 }
 
-// Per-column outer-iteration bookkeeping (solver.py:693-715).
-// sums[0..KC) = sum(R), sums[KC..2KC) = sum(R^2).
+// Per-column outer-iteration bookkeeping (solver.py:693-715) on the device,
+// plus the
+// check counter, the V-cycle tallies and the while-condition of the solve
+// graph.  Check c (0-based) is a regular check for c < max_cycles and the
+// reference's loop-exhausted final check for c == max_cycles.
+struct LoopCtl {
+    int* iter;               // checks done
+    long long* vcyc;         // column V-cycles executed
+    int* ncyc;               // block V-cycles executed
+};
 template <int KC>
-__global__ void k_status(int n, const double* __restrict__ sums, const double* __restrict__ bn,
-                         double* __restrict__ res, double* __restrict__ prev,
-                         int* __restrict__ stall, int* __restrict__ state,
-                         double* __restrict__ mean, int* __restrict__ count, double stop,
-                         double sfac, int scyc, int final_check) {
-    int c = threadIdx.x;
+__global__ void k_status_loop(int n, const double* __restrict__ sums,
+                              const double* __restrict__ bn, double* __restrict__ res,
+                              double* __restrict__ prev, int* __restrict__ stall,
+                              int* __restrict__ state, double* __restrict__ mean,
+                              int* __restrict__ count, double stop, double sfac, int scyc,
+                              int max_cycles, LoopCtl ctl, cudaGraphConditionalHandle cond,
+                              int use_cond) {
+    const int c = threadIdx.x;
+    const int check = *ctl.iter;
+    const bool final_check = check >= max_cycles;
     int a = 0;
     if (c < KC) {
-    if (state[c] == COL_ACTIVE) {
-        double r = sqrt(sums[KC + c]) / bn[c];
-        res[c] = r;
-        bool conv = r <= stop;
-        if (!final_check) {
-            double f = r / prev[c];
-            stall[c] = f > sfac ? stall[c] + 1 : 0;
-            prev[c] = r;
-            bool stuck = stall[c] >= scyc;
-            if (conv)
-                state[c] = COL_CONV;
-            else if (stuck)
-                state[c] = COL_FALLBACK;
-        } else {
-            state[c] = conv ? COL_CONV : COL_FALLBACK;
+        if (state[c] == COL_ACTIVE) {
+            double r = sqrt(sums[KC + c]) / bn[c];
+            res[c] = r;
+            bool conv = r <= stop;
+            if (!final_check) {
+                double f = r / prev[c];
+                stall[c] = f > sfac ? stall[c] + 1 : 0;
+                prev[c] = r;
+                if (conv)
+                    state[c] = COL_CONV;
+                else if (stall[c] >= scyc)
+                    state[c] = COL_FALLBACK;
+            } else {
+                state[c] = conv ? COL_CONV : COL_FALLBACK;
+            }
         }
+        mean[c] = sums[c] / (double)n;
+        a = (state[c] == COL_ACTIVE) ? 1 : 0;
     }
-    mean[c] = sums[c] / (double)n;
-    a = (state[c] == COL_ACTIVE) ? 1 : 0;
-    }
-    // deterministic count (integer)
     a = __syncthreads_count(a);
-    if (c == 0) *count = a;
+    if (c == 0) {
+        *count = a;
+        *ctl.iter = check + 1;
+        const bool go = a > 0;  // a == 0 after a final check
+        if (go) {
+            *ctl.vcyc += a;
+            *ctl.ncyc += 1;
+        }
+        if (use_cond) cudaGraphSetConditional(cond, go ? 1u : 0u);
+    }
+}
+
+template <int KC>
+__global__ void __launch_bounds__(kThreads) k_zero_block(int64_t elems, double* __restrict__ X) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < elems) X[t] = 0.0;
 }
 
 // R -= mean (per column)  (solver.py:567-568 _center)
@@ -949,6 +974,10 @@ struct Ops {
         k_lincomb<KC><<<grid_rows<KC>(h.n0), kThreads, 0, h.s>>>(h.n0, Y, U, W, coef);
     }
 
+    static void zero_block(Hier& h, double* x, int64_t elems) {
+        k_zero_block<KC><<<(unsigned)((elems + kThreads - 1) / kThreads), kThreads, 0, h.s>>>(elems,
+                                                                                          x);
+    }
     static double* bufb(Hier& h, int j) { return j == 0 ? h.R : h.L[j].b; }
     static double* bufx(Hier& h, int j) { return j == 0 ? h.C : h.L[j].x; }
 
@@ -960,7 +989,7 @@ struct Ops {
         if (l.kind == CF_LEVEL_COARSEST) {
             if (l.n == 1 || !l.M) {
                 ProfScope ps(h, "memset", j, Vb(l.n));
-                CF_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * (size_t)l.n * KC, h.s));
+                zero_block(h, x, (int64_t)l.n * KC);
             } else {
                 ProfScope ps(h, "dense", j, 8.0 * l.n * l.n + 2 * Vb(l.n));
                 const int S = dense_splits(l.n), chunk = dense_chunk(l.n, S);
@@ -997,7 +1026,7 @@ struct Ops {
         // aggregation level
         {
             ProfScope ps(h, "memset", j, Vb(l.n));
-            CF_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * (size_t)l.n * KC, h.s));
+            zero_block(h, x, (int64_t)l.n * KC);
         }
         for (int s = 0; s < nu1; ++s) {
             for (int col = 0; col < l.gs_classes; ++col) sweep(h, l, col, b, x, s == 0 && col == 0);
@@ -1075,6 +1104,69 @@ struct Ops {
         ProfScope ps(h, "jacobi_scatter", lev, Vb(2 * cnt) + 4.0 * cnt);
         k_scatter_rows<KC><<<grid_rows<KC>(cnt), kThreads, 0, h.s>>>(
             l.contig ? nullptr : l.crows + beg, beg, cnt, h.T, x);
+    }
+
+    // The whole outer iteration as one CUDA graph: a while node whose body is
+    // centre -> V-cycle -> update -> residual -> status; the status kernel sets
+    // the loop condition, so no host round trip happens between iterations.
+    static cudaGraphExec_t loop_graph(Hier& h, const CfSolveParams& p) {
+        const int key = KC * 1000000 + p.nu1 * 1000 + p.nu2;
+        auto it = h.loop_graphs.find(key);
+        if (it != h.loop_graphs.end()) return it->second;
+        cudaGraph_t g;
+        CF_CUDA(cudaGraphCreate(&g, 0));
+        cudaGraphConditionalHandle hc;
+        CF_CUDA(cudaGraphConditionalHandleCreate(&hc, g, 1, cudaGraphCondAssignDefault));
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = hc;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t node;
+        CF_CUDA(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        CF_CUDA(cudaStreamBeginCaptureToGraph(h.s, body, nullptr, nullptr, 0,
+                                              cudaStreamCaptureModeThreadLocal));
+        try {
+            issue_iteration(h, p, hc, 1);
+        } catch (...) {
+            cudaGraph_t tmp;
+            cudaStreamEndCapture(h.s, &tmp);
+            cudaGraphDestroy(g);
+            throw;
+        }
+        cudaGraph_t captured;
+        CF_CUDA(cudaStreamEndCapture(h.s, &captured));
+        cudaGraphExec_t ge;
+        CF_CUDA(cudaGraphInstantiate(&ge, g, 0));
+        CF_CUDA(cudaGraphDestroy(g));
+        h.loop_graphs.emplace(key, ge);
+        return ge;
+    }
+    // one outer iteration after a check: centre, cycle, update, next check
+    static void issue_iteration(Hier& h, const CfSolveParams& p, cudaGraphConditionalHandle hc,
+                                int use_cond) {
+        const int n = h.n0;
+        double* mean = h.sums + 2 * KC;
+        double* csum = h.sums + 3 * KC;
+        center(h, h.R, mean);
+        cycle(h, 0, p.nu1, p.nu2);
+        colsum(h, h.X, h.C, csum);
+        {
+            ProfScope ps(h, "update", 0, 3.0 * 8.0 * KC * n);
+            k_update<KC><<<grid_rows<KC>(n), kThreads, 0, h.s>>>(n, h.X, h.C, csum, h.state);
+        }
+        residual(h, h.B, h.X, h.R, h.sums);
+        status(h, p, hc, use_cond);
+    }
+    static void status(Hier& h, const CfSolveParams& p, cudaGraphConditionalHandle hc,
+                       int use_cond) {
+        ProfScope ps(h, "status", 0, 0.0);
+        LoopCtl ctl{h.d_iter, h.d_vcyc, h.d_ncyc};
+        k_status_loop<KC><<<1, KC < 32 ? 32 : KC, 0, h.s>>>(
+            h.n0, h.sums, h.bn, h.res, h.prev, h.stall, h.state, h.sums + 2 * KC, h.count,
+            p.stop_margin * p.tau, p.stagnation_factor, p.stagnation_cycles, p.max_cycles, ctl, hc,
+            use_cond);
     }
 
     static void run_cycle(Hier& h, int nu1, int nu2) {
@@ -1376,39 +1468,34 @@ static void solve_block_t(Hier& h, int ncols, const CfSolveParams& p, double* re
     double* csum = h.sums + 3 * KC;
     int64_t fallback_cols = 0;
     if (nactive > 0) {
-        bool broke = false;
-        for (int it = 0; it < p.max_cycles; ++it) {
-            O::residual(h, h.B, h.X, h.R, h.sums);
-            {
-                ProfScope ps(h, "status", 0, 0.0);
-                k_status<KC><<<1, KC < 32 ? 32 : KC, 0, h.s>>>(
-                    n, h.sums, h.bn, h.res, h.prev, h.stall, h.state, mean, h.count, stop,
-                    p.stagnation_factor, p.stagnation_cycles, 0);
+        // check 0 on the host path, then the device-controlled loop
+        CF_CUDA(cudaMemsetAsync(h.d_iter, 0, sizeof(int), h.s));
+        CF_CUDA(cudaMemsetAsync(h.d_vcyc, 0, sizeof(long long), h.s));
+        CF_CUDA(cudaMemsetAsync(h.d_ncyc, 0, sizeof(int), h.s));
+        O::residual(h, h.B, h.X, h.R, h.sums);
+        O::status(h, p, cudaGraphConditionalHandle{}, 0);
+        CF_CUDA(cudaMemcpyAsync(h.h_count, h.count, sizeof(int), cudaMemcpyDeviceToHost, h.s));
+        CF_CUDA(cudaStreamSynchronize(h.s));
+        if (*h.h_count > 0) {
+            if (h.prof) {
+                // eager loop so every kernel is bracketed by events
+                for (int it = 0; it <= p.max_cycles && *h.h_count > 0; ++it) {
+                    O::issue_iteration(h, p, cudaGraphConditionalHandle{}, 0);
+                    CF_CUDA(cudaMemcpyAsync(h.h_count, h.count, sizeof(int),
+                                            cudaMemcpyDeviceToHost, h.s));
+                    CF_CUDA(cudaStreamSynchronize(h.s));
+                }
+            } else {
+                CF_CUDA(cudaGraphLaunch(O::loop_graph(h, p), h.s));
             }
-            CF_CUDA(cudaMemcpyAsync(h.h_count, h.count, sizeof(int), cudaMemcpyDeviceToHost, h.s));
-            CF_CUDA(cudaStreamSynchronize(h.s));
-            int act = *h.h_count;
-            if (act == 0) {
-                broke = true;
-                break;
-            }
-            O::center(h, h.R, mean);
-            O::run_cycle(h, p.nu1, p.nu2);
-            O::colsum(h, h.X, h.C, csum);
-            {
-                ProfScope ps(h, "update", 0, 3.0 * 8.0 * KC * n);
-                k_update<KC><<<grid_rows<KC>(n), kThreads, 0, h.s>>>(n, h.X, h.C, csum, h.state);
-            }
-            st.vcycles += act;
-            st.outer_iterations += 1;
         }
-        if (!broke) {
-            O::residual(h, h.B, h.X, h.R, h.sums);
-            k_status<KC><<<1, KC < 32 ? 32 : KC, 0, h.s>>>(n, h.sums, h.bn, h.res, h.prev, h.stall,
-                                                            h.state, mean, h.count, stop,
-                                                            p.stagnation_factor,
-                                                            p.stagnation_cycles, 1);
-        }
+        long long vc = 0;
+        int nc = 0;
+        CF_CUDA(cudaMemcpyAsync(&vc, h.d_vcyc, sizeof(long long), cudaMemcpyDeviceToHost, h.s));
+        CF_CUDA(cudaMemcpyAsync(&nc, h.d_ncyc, sizeof(int), cudaMemcpyDeviceToHost, h.s));
+        CF_CUDA(cudaStreamSynchronize(h.s));
+        st.vcycles += vc;
+        st.outer_iterations += nc;
         CF_CUDA(cudaMemcpyAsync(state.data(), h.state, sizeof(int) * KC, cudaMemcpyDeviceToHost,
                                 h.s));
         CF_CUDA(cudaMemcpyAsync(res.data(), h.res, sizeof(double) * KC, cudaMemcpyDeviceToHost,
@@ -1547,6 +1634,7 @@ void* Hier::dalloc(size_t nb) {
 Hier::~Hier() {
     cudaSetDevice(dev);
     for (auto& kv : cycle_graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& kv : loop_graphs) cudaGraphExecDestroy(kv.second);
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     for (void* p : owned) cudaFree(p);
     for (auto& l : L) {
@@ -1578,6 +1666,8 @@ void Hier::ensure_workspace(int kc) {
     if (kc <= kc_ws) return;
     for (auto& kv : cycle_graphs) cudaGraphExecDestroy(kv.second);
     cycle_graphs.clear();
+    for (auto& kv : loop_graphs) cudaGraphExecDestroy(kv.second);
+    loop_graphs.clear();
     CF_CUDA(cudaStreamSynchronize(s));
     auto re = [&](double*& p, size_t elems) {
         if (p) {
@@ -1903,6 +1993,9 @@ extern "C" int cf_hier_create(int32_t nlev, const CfLevelDesc* ds, int32_t devic
         h->stall = (int*)h->dalloc(sizeof(int) * kMaxKC);
         h->state = (int*)h->dalloc(sizeof(int) * kMaxKC);
         h->count = (int*)h->dalloc(sizeof(int) * 4);
+        h->d_iter = (int*)h->dalloc(sizeof(int) * 4);
+        h->d_ncyc = (int*)h->dalloc(sizeof(int) * 4);
+        h->d_vcyc = (long long*)h->dalloc(sizeof(long long) * 2);
         CF_CUDA(cudaMallocHost(&h->h_count, sizeof(int) * 4));
         CF_CUDA(cudaMallocHost(&h->h_small, sizeof(double) * 16 * kMaxKC));
     } catch (...) {
