@@ -272,25 +272,28 @@ def run_gpu_arm(args):
         for kind, lv, la, kms, by in sorted(rep, key=lambda r: -r[3]):
             f.write(f"{kind} {lv} {la} {kms:.4f} {by:.0f} {by / max(kms, 1e-9) / 1e6:.1f}\n")
     kinds = {}
+    inst = {}
     launches = 0
     for kind, lv, la, kms, by in rep:
         a = kinds.setdefault(kind, [0, 0.0, 0.0])
         a[0] += la
         a[1] += kms
         a[2] += by
+        inst[f"{kind}@L{lv}"] = (la, kms, by)
         if kind != "memset":
             launches += la
     prof_ms = sum(v[1] for v in kinds.values())
-    dom = max(kinds.items(), key=lambda kv: kv[1][1])
+    # dominant kernel instance: (kind, level) with the largest total time
+    dom_name, (dom_la, dom_ms, dom_by) = max(inst.items(), key=lambda kv: kv[1][1])
     peak, peak_src = _peaks()
-    dom_bytes_per_launch = dom[1][2] / dom[1][0]
-    dom_ms_per_launch = dom[1][1] / dom[1][0]
+    dom_bytes_per_launch = dom_by / dom_la
+    dom_ms_per_launch = dom_ms / dom_la
     achieved = dom_bytes_per_launch / (dom_ms_per_launch * 1e-3) / 1e9
     traffic = None
     tfile = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(tfile):
         with open(tfile) as f:
-            traffic = json.load(f).get(dom[0])
+            traffic = json.load(f).get(dom_name)
     total_bytes = sum(v[2] for v in kinds.values())
 
     # --- e2e through the public API with host buffers (same right-hand sides)
@@ -352,7 +355,7 @@ def run_gpu_arm(args):
                        "parallelism": f"sketch rows sharded over {world} GPU(s)",
                        "l2": "working set (per-level b,x blocks) larger than the 126 MB L2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": dom[0],
+                         "frac": achieved / peak, "traffic": traffic, "kernel": dom_name,
                          "peak_source": peak_src,
                          "bytes_per_launch": dom_bytes_per_launch,
                          "ms_per_launch": dom_ms_per_launch},

@@ -112,6 +112,7 @@ struct Hier {
     int *d_iter = nullptr, *d_ncyc = nullptr;
     long long* d_vcyc = nullptr;
     bool prof = false;
+    bool host_loop = false;  // CF_HOST_LOOP=1
     std::vector<ProfRec> recs;
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;

@@ -18,7 +18,10 @@ namespace cf {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kRowsPerPart = 64;
+#ifndef CF_ROWS_PER_PART
+#define CF_ROWS_PER_PART 64
+#endif
+constexpr int kRowsPerPart = CF_ROWS_PER_PART;
 #ifndef CF_GATHER_CTAS
 #define CF_GATHER_CTAS 3
 #endif

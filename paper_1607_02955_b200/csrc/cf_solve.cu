@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -23,6 +24,10 @@
 #include "cf_hier.h"
 #include "cf_kernels.cuh"
 #include "cfcent_b200.h"
+
+#ifndef CF_RED_CTAS
+#define CF_RED_CTAS 3  // min CTAs/SM for the reduction / restriction gather kernels
+#endif
 
 namespace cf {
 
@@ -48,7 +53,7 @@ enum ColState { COL_ZERO = 0, COL_ACTIVE = 1, COL_CONV = 2, COL_FALLBACK = 3 };
 
 // R = B - L X ; partials of sum(R), sum(R^2)  (solver.py:694-695)
 template <int KC>
-__global__ void __launch_bounds__(kThreads, 2) k_residual(int n, const int64_t* __restrict__ rp,
+__global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : CF_RED_CTAS)) k_residual(int n, const int64_t* __restrict__ rp,
                                                        const int32_t* __restrict__ col,
                                                        const double* __restrict__ val,
                                                        const double* __restrict__ diag,
@@ -86,7 +91,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_residual(int n, const int64_t* 
 
 // Y = L X (full Laplacian product) -- fallback Krylov solvers (solver.py:571-648)
 template <int KC>
-__global__ void __launch_bounds__(kThreads, 2) k_spmm(int n, const int64_t* __restrict__ rp,
+__global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : CF_RED_CTAS)) k_spmm(int n, const int64_t* __restrict__ rp,
                                                    const int32_t* __restrict__ col,
                                                    const double* __restrict__ val,
                                                    const double* __restrict__ diag,
@@ -563,7 +568,7 @@ __global__ void __launch_bounds__(kThreads) k_scatter_rows(const int32_t* __rest
 
 // bc[a] = sum_{i in a} (b_i - L_i x)  (residual fused with P^T, solver.py:548-549)
 template <int KC>
-__global__ void __launch_bounds__(kThreads, 2) k_agg_restrict(
+__global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : CF_RED_CTAS)) k_agg_restrict(
     int nc, const int32_t* __restrict__ aptr, const int32_t* __restrict__ amem,
     const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
     const double* __restrict__ val, const double* __restrict__ diag,
@@ -590,7 +595,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_agg_restrict(
 // Line-search partials (solver.py:550-556): den = d . L d with d = P xc over
 // fine rows (CTAs [0, pf)), num = r . d = bc . xc over coarse rows (CTAs [pf, pf+pc)).
 template <int KC>
-__global__ void __launch_bounds__(kThreads, 2) k_agg_ls(
+__global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : CF_RED_CTAS)) k_agg_ls(
     int n, int nc, const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
     const double* __restrict__ val, const double* __restrict__ diag,
     const int32_t* __restrict__ agg, const double* __restrict__ Xc,
@@ -652,7 +657,7 @@ __global__ void __launch_bounds__(kThreads) k_agg_correct(int n, const int32_t* 
 
 // bc_i = b[c_i] + sum_f W_cf(i,f) * (b_f / d_f)  (solver.py:534-536)
 template <int KC>
-__global__ void __launch_bounds__(kThreads, 2) k_elim_restrict(
+__global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : CF_RED_CTAS)) k_elim_restrict(
     int nc, const int32_t* __restrict__ cn, const int64_t* __restrict__ wp,
     const int32_t* __restrict__ wc, const double* __restrict__ wv,
     const int32_t* __restrict__ fn, const double* __restrict__ fd,
@@ -1477,7 +1482,7 @@ static void solve_block_t(Hier& h, int ncols, const CfSolveParams& p, double* re
         CF_CUDA(cudaMemcpyAsync(h.h_count, h.count, sizeof(int), cudaMemcpyDeviceToHost, h.s));
         CF_CUDA(cudaStreamSynchronize(h.s));
         if (*h.h_count > 0) {
-            if (h.prof) {
+            if (h.prof || h.host_loop) {
                 // eager loop so every kernel is bracketed by events
                 for (int it = 0; it <= p.max_cycles && *h.h_count > 0; ++it) {
                     O::issue_iteration(h, p, cudaGraphConditionalHandle{}, 0);
@@ -1993,6 +1998,9 @@ extern "C" int cf_hier_create(int32_t nlev, const CfLevelDesc* ds, int32_t devic
         h->stall = (int*)h->dalloc(sizeof(int) * kMaxKC);
         h->state = (int*)h->dalloc(sizeof(int) * kMaxKC);
         h->count = (int*)h->dalloc(sizeof(int) * 4);
+        // CF_HOST_LOOP=1: drive the outer iteration from the host (profilers
+        // cannot attribute kernels inside graphs with conditional nodes)
+        if (const char* e = std::getenv("CF_HOST_LOOP")) h->host_loop = std::atoi(e) != 0;
         h->d_iter = (int*)h->dalloc(sizeof(int) * 4);
         h->d_ncyc = (int*)h->dalloc(sizeof(int) * 4);
         h->d_vcyc = (long long*)h->dalloc(sizeof(long long) * 2);

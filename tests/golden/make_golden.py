@@ -185,6 +185,42 @@ def config2():
     save("config2.npz", **d)
 
 
+def config3(tau_list=(1e-6, 1e-10)):
+    """C3: RGG 1e6 (recipe of paper_1607_02955_b200/configs.py, restated here
+    with the reference's own Graph/LCC); JL k=128 (Q seed 0) and sampling 256
+    pivots (seed 3) for the max-degree node."""
+    from scipy.spatial import cKDTree
+    n = 1_000_000
+    pts = np.random.default_rng(3).random((n, 2))
+    r = math.sqrt(10.0 / (math.pi * n))
+    pairs = cKDTree(pts).query_pairs(r, output_type="ndarray")
+    dist = np.linalg.norm(pts[pairs[:, 0]] - pts[pairs[:, 1]], axis=1)
+    g0 = cfcent.Graph.from_edges(pairs[:, 0], pairs[:, 1], 1.0 / (dist + 1e-3), n=n)
+    g, _ = cfcent.largest_connected_component(g0)
+    deg = np.diff(g.indptr)
+    u = int(np.argmax(deg))
+    eps = math.sqrt(math.log(g.n) / 127.5)
+    d = {"n": np.int64(g.n), "m": np.int64(g.m), "u": np.int64(u), "eps": np.float64(eps)}
+    for tau in tau_list:
+        cfg = slv.SolverConfig(tau=tau, seed=0)
+        t0 = time.perf_counter()
+        h = slv.setup(cfcent.laplacian(g), cfg)
+        t1 = time.perf_counter()
+        jl = cfcent.cf_closeness_projection(g, h, [u], eps, 0, cfg, threads=2)
+        t2 = time.perf_counter()
+        sm = cfcent.cf_closeness_sampling(g, h, [u], 256, 3, cfg, threads=5)
+        t3 = time.perf_counter()
+        tag = f"{tau:.0e}".replace("-", "m")
+        d[f"sizes"] = np.array(h.level_sizes)
+        d[f"jl_{tag}"] = jl.vector([u])
+        d[f"samp_{tag}"] = sm.vector([u])
+        d[f"t_setup_{tag}"] = np.float64(t1 - t0)
+        d[f"t_jl_{tag}"] = np.float64(t2 - t1)
+        d[f"t_samp_{tag}"] = np.float64(t3 - t2)
+        print("C3", tau, jl.vector([u]), sm.vector([u]), t1 - t0, t2 - t1, t3 - t2, flush=True)
+        save("config3.npz", **d)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["kats", "small", "c1", "c2"]
     if "kats" in which:
@@ -195,3 +231,5 @@ if __name__ == "__main__":
         config1()
     if "c2" in which:
         config2()
+    if "c3" in which:
+        config3()
