@@ -752,7 +752,9 @@ __global__ void __launch_bounds__(kThreads) k_dense_small(int n, int chunk,
 }
 
 // wide blocks: 128 x TC output tile per CTA (TC = min(KC,128)), 16-deep l
-// stages in shared memory, 8 x (TC/16) register tile per thread.
+// stages in shared memory, 8 x (TC/16) register tile per thread; the next
+// stage's tiles are prefetched into registers while the current one is
+// multiplied (global-load latency overlapped with the fp64 FMAs).
 constexpr int kGR = 128, kGL = 16;
 template <int KC>
 __global__ void __launch_bounds__(kThreads) k_dense_tile(int n, int chunk,
@@ -761,6 +763,8 @@ __global__ void __launch_bounds__(kThreads) k_dense_tile(int n, int chunk,
                                                          double* __restrict__ P) {
     constexpr int TC = KC < 128 ? KC : 128;
     constexpr int CT = TC / 16;
+    constexpr int NA = kGR * kGL / kThreads;  // A elements per thread per stage
+    constexpr int NB = kGL * TC / kThreads;   // B elements per thread per stage
     __shared__ double sA[kGL][kGR + 2];
     __shared__ double sB[kGL][TC];
     const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
@@ -771,18 +775,35 @@ __global__ void __launch_bounds__(kThreads) k_dense_tile(int n, int chunk,
     for (int r = 0; r < 8; ++r)
 #pragma unroll
         for (int c = 0; c < CT; ++c) acc[r][c] = 0.0;
-    for (int lb = l0; lb < l1; lb += kGL) {
-        for (int e = tid; e < kGR * kGL; e += kThreads) {
-            const int r = e / kGL, t = e % kGL;
+    double ra[NA], rb[NB > 0 ? NB : 1];
+    auto fetch = [&](int lb) {
+#pragma unroll
+        for (int q = 0; q < NA; ++q) {
+            const int e = tid + q * kThreads, r = e / kGL, t = e % kGL;
             const int i = i0 + r, l = lb + t;
-            sA[t][r] = (i < n && l < l1) ? __ldg(M + (size_t)i * n + l) : 0.0;
+            ra[q] = (i < n && l < l1) ? __ldg(M + (size_t)i * n + l) : 0.0;
         }
-        for (int e = tid; e < kGL * TC; e += kThreads) {
-            const int t = e / TC, c = e % TC;
+#pragma unroll
+        for (int q = 0; q < NB; ++q) {
+            const int e = tid + q * kThreads, t = e / TC, c = e % TC;
             const int l = lb + t;
-            sB[t][c] = (l < l1) ? __ldg(B + (size_t)l * KC + j0 + c) : 0.0;
+            rb[q] = (l < l1) ? __ldg(B + (size_t)l * KC + j0 + c) : 0.0;
+        }
+    };
+    if (l0 < l1) fetch(l0);
+    for (int lb = l0; lb < l1; lb += kGL) {
+#pragma unroll
+        for (int q = 0; q < NA; ++q) {
+            const int e = tid + q * kThreads;
+            sA[e % kGL][e / kGL] = ra[q];
+        }
+#pragma unroll
+        for (int q = 0; q < NB; ++q) {
+            const int e = tid + q * kThreads;
+            sB[e / TC][e % TC] = rb[q];
         }
         __syncthreads();
+        if (lb + kGL < l1) fetch(lb + kGL);
         const int tmax = min(kGL, l1 - lb);
         for (int t = 0; t < tmax; ++t) {
             double a[8], bb[CT];
