@@ -14,7 +14,48 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+#include <string>
+#include <utility>
+
+// Programmatic dependent launch (sm_90+): every kernel first waits for the
+// grid it depends on (no-op without a programmatic dependency), then lets its
+// own dependents start launching, so a dependent kernel's launch and prologue
+// overlap the tail of this one.
+#define CF_PDL_ENTRY()                                      \
+    do {                                                    \
+        asm volatile("griddepcontrol.wait;" ::: "memory");  \
+        asm volatile("griddepcontrol.launch_dependents;");  \
+    } while (0)
+
 namespace cf {
+
+inline bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("CF_PDL");
+        return !e || std::atoi(e) != 0;
+    }();
+    return on;
+}
+
+// kernel launch with the programmatic-stream-serialization attribute
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                     cudaStream_t stream, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+    if (e != cudaSuccess)
+        throw std::runtime_error(std::string("kernel launch failed: ") + cudaGetErrorString(e));
+}
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;

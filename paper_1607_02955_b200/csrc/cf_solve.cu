@@ -62,6 +62,7 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : CF_RED_CTAS)) k_res
                                                        double* __restrict__ R,
                                                        double* __restrict__ parts,
                                                        int64_t nparts, HeavyDev H) {
+    CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
     extern __shared__ double smem[];
     DV<V> loc[2];
@@ -97,6 +98,7 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : CF_RED_CTAS)) k_spm
                                                    const double* __restrict__ diag,
                                                    const double* __restrict__ X,
                                                    double* __restrict__ Y, HeavyDev H) {
+    CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
     int64_t i = (int64_t)blockIdx.x * Lt::RPB + slot;
     if (i >= n || !lane_ok) return;
@@ -115,6 +117,7 @@ template <int KC>
 __global__ void __launch_bounds__(kThreads) k_colstats(int n, const double* __restrict__ B,
                                                        double* __restrict__ parts,
                                                        int64_t nparts) {
+    CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
     extern __shared__ double smem[];
     DV<V> loc[3];
@@ -143,6 +146,7 @@ __global__ void __launch_bounds__(kThreads) k_dot2(int n, const double* __restri
                                                    const double* __restrict__ U2,
                                                    const double* __restrict__ V2,
                                                    double* __restrict__ parts, int64_t nparts) {
+    CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
     extern __shared__ double smem[];
     DV<V> loc[2];
@@ -169,6 +173,7 @@ __global__ void __launch_bounds__(kThreads) k_colsum(int n, const double* __rest
                                                      const double* __restrict__ Y,
                                                      double* __restrict__ parts,
                                                      int64_t nparts) {
+    CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
     extern __shared__ double smem[];
     DV<V> loc[1];
@@ -200,6 +205,7 @@ template <int KC>
 __global__ void __launch_bounds__(kThreads) k_fin1(const double* __restrict__ parts,
                                                    int64_t nparts, int64_t qstride,
                                                    double* __restrict__ out1, int64_t nseg) {
+    CF_PDL_ENTRY();
     const int q = blockIdx.y;
     const int64_t seg = blockIdx.x;
     const double* p0 = parts + (size_t)q * qstride;
@@ -214,6 +220,7 @@ __global__ void __launch_bounds__(kThreads) k_fin1(const double* __restrict__ pa
 template <int KC>
 __global__ void __launch_bounds__(kThreads) k_fin2(const double* __restrict__ in, int64_t cnt,
                                                    int64_t qstride, double* __restrict__ out) {
+    CF_PDL_ENTRY();
     const int q = blockIdx.x;
     for (int c = threadIdx.x; c < KC; c += blockDim.x) {
         double t = 0.0;
@@ -240,6 +247,7 @@ __global__ void k_status_loop(int n, const double* __restrict__ sums,
                               int* __restrict__ count, double stop, double sfac, int scyc,
                               int max_cycles, LoopCtl ctl, cudaGraphConditionalHandle cond,
                               int use_cond) {
+    CF_PDL_ENTRY();
     const int c = threadIdx.x;
     const int check = *ctl.iter;
     const bool final_check = check >= max_cycles;
@@ -279,6 +287,7 @@ __global__ void k_status_loop(int n, const double* __restrict__ sums,
 
 template <int KC>
 __global__ void __launch_bounds__(kThreads) k_zero_block(int64_t elems, double* __restrict__ X) {
+    CF_PDL_ENTRY();
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t < elems) X[t] = 0.0;
 }
@@ -287,6 +296,7 @@ __global__ void __launch_bounds__(kThreads) k_zero_block(int64_t elems, double* 
 template <int KC>
 __global__ void __launch_bounds__(kThreads) k_center(int n, double* __restrict__ R,
                                                      const double* __restrict__ mean) {
+    CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
     int64_t i = (int64_t)blockIdx.x * Lt::RPB + slot;
     if (i >= n || !lane_ok) return;
@@ -302,6 +312,7 @@ __global__ void __launch_bounds__(kThreads) k_update(int n, double* __restrict__
                                                      const double* __restrict__ C,
                                                      const double* __restrict__ csum,
                                                      const int* __restrict__ state) {
+    CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
     int64_t i = (int64_t)blockIdx.x * Lt::RPB + slot;
     if (i >= n || !lane_ok) return;
@@ -318,6 +329,7 @@ __global__ void __launch_bounds__(kThreads) k_lincomb(int n, double* __restrict_
                                                       const double* __restrict__ U,
                                                       const double* __restrict__ W,
                                                       const double* __restrict__ coef) {
+    CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
     int64_t i = (int64_t)blockIdx.x * Lt::RPB + slot;
     if (i >= n || !lane_ok) return;
@@ -350,6 +362,7 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : kGatherCtas)) k_gs(
                                                               double* __restrict__ X,
                                                               int from_zero, HeavyDev H,
                                                               SegWork w) {
+    CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
     int64_t g = (int64_t)blockIdx.x * Lt::RPB + slot;
     if (!lane_ok) return;
@@ -404,6 +417,7 @@ __global__ void __launch_bounds__(kThreads, CF_PIPE_CTAS)
                  const double* __restrict__ val, const double* __restrict__ diag,
                  const double* __restrict__ B, double* __restrict__ X, double* __restrict__ T,
                  int from_zero, HeavyDev H, SegWork w) {
+    CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
     constexpr int W = Lt::LPR;
     constexpr unsigned MASK = W == 32 ? 0xffffffffu : ((1u << W) - 1u);
@@ -522,6 +536,7 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : kGatherCtas)) k_jac
     const int32_t* __restrict__ col, const double* __restrict__ val,
     const double* __restrict__ diag, const double* __restrict__ B, const double* __restrict__ X,
     double* __restrict__ T, HeavyDev H, SegWork w) {
+    CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
     int64_t g = (int64_t)blockIdx.x * Lt::RPB + slot;
     if (!lane_ok) return;
@@ -559,6 +574,7 @@ __global__ void __launch_bounds__(kThreads) k_scatter_rows(const int32_t* __rest
                                                            int base, int cnt,
                                                            const double* __restrict__ T,
                                                            double* __restrict__ X) {
+    CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
     int64_t g = (int64_t)blockIdx.x * Lt::RPB + slot;
     if (g >= cnt || !lane_ok) return;
@@ -574,6 +590,7 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : CF_RED_CTAS)) k_agg
     const double* __restrict__ val, const double* __restrict__ diag,
     const double* __restrict__ B, const double* __restrict__ X, double* __restrict__ Bc,
     HeavyDev H) {
+    CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
     int64_t a = (int64_t)blockIdx.x * Lt::RPB + slot;
     if (a >= nc || !lane_ok) return;
@@ -601,6 +618,7 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : CF_RED_CTAS)) k_agg
     const int32_t* __restrict__ agg, const double* __restrict__ Xc,
     const double* __restrict__ Bc, double* __restrict__ pden, int64_t pf,
     double* __restrict__ pnum, int64_t pc, HeavyDev H) {
+    CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
     extern __shared__ double smem[];
     DV<V> loc[1];
@@ -641,6 +659,7 @@ __global__ void __launch_bounds__(kThreads) k_agg_correct(int n, const int32_t* 
                                                           double* __restrict__ X,
                                                           const double* __restrict__ Xc,
                                                           const double* __restrict__ ls) {
+    CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
     int64_t i = (int64_t)blockIdx.x * Lt::RPB + slot;
     if (i >= n || !lane_ok) return;
@@ -662,6 +681,7 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : CF_RED_CTAS)) k_eli
     const int32_t* __restrict__ wc, const double* __restrict__ wv,
     const int32_t* __restrict__ fn, const double* __restrict__ fd,
     const double* __restrict__ B, double* __restrict__ Bc, HeavyDev H) {
+    CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
     int64_t i = (int64_t)blockIdx.x * Lt::RPB + slot;
     if (i >= nc || !lane_ok) return;
@@ -685,6 +705,7 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : kGatherCtas)) k_seg
                                                   const double* __restrict__ div,
                                                   const double* __restrict__ X,
                                                   double* __restrict__ P) {
+    CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
     int64_t sg = s_lo + (int64_t)blockIdx.x * Lt::RPB + slot;
     if (sg >= s_hi || !lane_ok) return;
@@ -701,6 +722,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_elim_interp(
     const int64_t* __restrict__ wp, const int32_t* __restrict__ wc,
     const double* __restrict__ wv, const double* __restrict__ fd,
     const double* __restrict__ B, const double* __restrict__ Xc, double* __restrict__ X) {
+    CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
     int64_t g = (int64_t)blockIdx.x * Lt::RPB + slot;
     if (!lane_ok) return;
@@ -740,6 +762,7 @@ __global__ void __launch_bounds__(kThreads) k_dense_small(int n, int chunk,
                                                           const double* __restrict__ M,
                                                           const double* __restrict__ B,
                                                           double* __restrict__ P) {
+    CF_PDL_ENTRY();
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int s = blockIdx.y;
     if (t >= (int64_t)n * KC) return;
@@ -761,6 +784,7 @@ __global__ void __launch_bounds__(kThreads) k_dense_tile(int n, int chunk,
                                                          const double* __restrict__ M,
                                                          const double* __restrict__ B,
                                                          double* __restrict__ P) {
+    CF_PDL_ENTRY();
     constexpr int TC = KC < 128 ? KC : 128;
     constexpr int CT = TC / 16;
     constexpr int NA = kGR * kGL / kThreads;  // A elements per thread per stage
@@ -832,6 +856,7 @@ template <int KC>
 __global__ void __launch_bounds__(kThreads) k_dense_reduce(int n, int S,
                                                            const double* __restrict__ P,
                                                            double* __restrict__ X) {
+    CF_PDL_ENTRY();
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= (int64_t)n * KC) return;
     double acc = 0.0;
@@ -844,6 +869,7 @@ __global__ void __launch_bounds__(kThreads) k_dense_reduce(int n, int S,
 template <int KC>
 __global__ void k_rows_to_block(const double* __restrict__ S, int cnt, int n,
                                 const int32_t* __restrict__ perm, double* __restrict__ B) {
+    CF_PDL_ENTRY();
     __shared__ double tile[32][33];
     int i0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
     int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
@@ -862,6 +888,7 @@ __global__ void k_rows_to_block(const double* __restrict__ S, int cnt, int n,
 template <int KC>
 __global__ void k_block_to_rows(const double* __restrict__ B, int cnt, int n,
                                 const int32_t* __restrict__ perm, double* __restrict__ S) {
+    CF_PDL_ENTRY();
     __shared__ double tile[32][33];
     int i0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
     int tx = threadIdx.x, ty = threadIdx.y;
@@ -881,6 +908,7 @@ __global__ void k_block_to_rows(const double* __restrict__ B, int cnt, int n,
 __global__ void k_permute_rows(const double* __restrict__ src, int ks, double* __restrict__ dst,
                                int kd, int k, int n, const int32_t* __restrict__ perm,
                                int gather) {
+    CF_PDL_ENTRY();
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= (int64_t)n * k) return;
     int64_t i = t / k;
@@ -912,12 +940,12 @@ static void finalize(Hier& h, const double* parts, int64_t nparts, int nq, int64
     ProfScope ps(h, "finalize", -1, 8.0 * KC * nq * (nparts + 1));
     const unsigned thr = KC < 32 ? 32 : (KC > kThreads ? kThreads : KC);
     if (nparts <= kFinSeg) {
-        k_fin2<KC><<<nq, thr, 0, h.s>>>(parts, nparts, qstride, out);
+        launch_k(k_fin2<KC>, dim3(nq), dim3(thr), 0, h.s, parts, nparts, qstride, out);
     } else {
         const int64_t nseg = (nparts + kFinSeg - 1) / kFinSeg;
-        k_fin1<KC><<<dim3((unsigned)nseg, nq), thr, 0, h.s>>>(parts, nparts, qstride, h.fin,
+        launch_k(k_fin1<KC>, dim3(dim3((unsigned)nseg, nq)), dim3(thr), 0, h.s, parts, nparts, qstride, h.fin,
                                                               nseg);
-        k_fin2<KC><<<nq, thr, 0, h.s>>>(h.fin, nseg, nseg * KC, out);
+        launch_k(k_fin2<KC>, dim3(nq), dim3(thr), 0, h.s, h.fin, nseg, nseg * KC, out);
     }
 }
 
@@ -956,15 +984,14 @@ struct Ops {
                     int level) {
         if (hi <= lo) return;
         ProfScope ps(h, "heavy_seg", level, 12.0 * kSegNnz * (hi - lo) + Vb(hi - lo) * 2);
-        k_seg<KC, MODE><<<(unsigned)((hi - lo + Lay<KC>::RPB - 1) / Lay<KC>::RPB), kThreads, 0,
-                          h.s>>>(lo, hi, pl.sbeg, pl.send, col, val, map, div, X, h.SP);
+        launch_k(k_seg<KC, MODE>, dim3((unsigned)((hi - lo + Lay<KC>::RPB - 1) / Lay<KC>::RPB)), dim3(kThreads), 0, h.s, lo, hi, pl.sbeg, pl.send, col, val, map, div, X, h.SP);
     }
     static void residual(Hier& h, const double* B, const double* X, double* R, double* sums2) {
         DLevel& l = h.L[0];
         int64_t np = nparts_of(l.n);
         seg<G_PLAIN>(h, l.pm, 0, l.pm.nseg, l.col, l.val, nullptr, nullptr, X, 0);
         ProfScope ps(h, "residual", 0, A(l.n, l.nnz) + Vb(l.n) * (R ? 3 : 2));
-        k_residual<KC><<<(unsigned)np, kThreads, red_smem<KC, 2>(), h.s>>>(
+        launch_k(k_residual<KC>, dim3((unsigned)np), dim3(kThreads), red_smem<KC, 2>(), h.s, 
             l.n, l.rp, l.col, l.val, l.diag, B, X, R, h.parts, np, hd(h, l.pm));
         finalize<KC>(h, h.parts, np, 2, np * KC, sums2);
     }
@@ -972,7 +999,7 @@ struct Ops {
         int n = h.n0;
         int64_t np = nparts_of(n);
         ProfScope ps(h, "colsum", 0, Vb(n) * (Y ? 2 : 1));
-        k_colsum<KC><<<(unsigned)np, kThreads, red_smem<KC, 1>(), h.s>>>(n, X, Y, h.parts, np);
+        launch_k(k_colsum<KC>, dim3((unsigned)np), dim3(kThreads), red_smem<KC, 1>(), h.s, n, X, Y, h.parts, np);
         finalize<KC>(h, h.parts, np, 1, np * KC, out);
     }
     static void dot2(Hier& h, const double* a, const double* b, const double* c, const double* d,
@@ -980,7 +1007,7 @@ struct Ops {
         int n = h.n0;
         int64_t np = nparts_of(n);
         ProfScope ps(h, "fallback", 0, 0.0);
-        k_dot2<KC><<<(unsigned)np, kThreads, red_smem<KC, 2>(), h.s>>>(n, a, b, c, d, h.parts,
+        launch_k(k_dot2<KC>, dim3((unsigned)np), dim3(kThreads), red_smem<KC, 2>(), h.s, n, a, b, c, d, h.parts,
                                                                       np);
         finalize<KC>(h, h.parts, np, 2, np * KC, out);
     }
@@ -988,20 +1015,20 @@ struct Ops {
         DLevel& l = h.L[0];
         seg<G_PLAIN>(h, l.pm, 0, l.pm.nseg, l.col, l.val, nullptr, nullptr, X, 0);
         ProfScope ps(h, "fallback", 0, 0.0);
-        k_spmm<KC><<<grid_rows<KC>(l.n), kThreads, 0, h.s>>>(l.n, l.rp, l.col, l.val, l.diag, X,
+        launch_k(k_spmm<KC>, dim3(grid_rows<KC>(l.n)), dim3(kThreads), 0, h.s, l.n, l.rp, l.col, l.val, l.diag, X,
                                                              Y, hd(h, l.pm));
     }
     static void center(Hier& h, double* X, const double* mean) {
         ProfScope ps(h, "center", 0, 2 * Vb(h.n0));
-        k_center<KC><<<grid_rows<KC>(h.n0), kThreads, 0, h.s>>>(h.n0, X, mean);
+        launch_k(k_center<KC>, dim3(grid_rows<KC>(h.n0)), dim3(kThreads), 0, h.s, h.n0, X, mean);
     }
     static void lincomb(Hier& h, double* Y, const double* U, const double* W, const double* coef) {
         ProfScope ps(h, "fallback", 0, 0.0);
-        k_lincomb<KC><<<grid_rows<KC>(h.n0), kThreads, 0, h.s>>>(h.n0, Y, U, W, coef);
+        launch_k(k_lincomb<KC>, dim3(grid_rows<KC>(h.n0)), dim3(kThreads), 0, h.s, h.n0, Y, U, W, coef);
     }
 
     static void zero_block(Hier& h, double* x, int64_t elems) {
-        k_zero_block<KC><<<(unsigned)((elems + kThreads - 1) / kThreads), kThreads, 0, h.s>>>(elems,
+        launch_k(k_zero_block<KC>, dim3((unsigned)((elems + kThreads - 1) / kThreads)), dim3(kThreads), 0, h.s, elems,
                                                                                           x);
     }
     static double* bufb(Hier& h, int j) { return j == 0 ? h.R : h.L[j].b; }
@@ -1021,13 +1048,12 @@ struct Ops {
                 const int S = dense_splits(l.n), chunk = dense_chunk(l.n, S);
                 if constexpr (KC >= 16) {
                     dim3 grd((unsigned)((l.n + kGR - 1) / kGR), KC / (KC < 128 ? KC : 128), S);
-                    k_dense_tile<KC><<<grd, kThreads, 0, h.s>>>(l.n, chunk, l.M, b, h.DP);
+                    launch_k(k_dense_tile<KC>, dim3(grd), dim3(kThreads), 0, h.s, l.n, chunk, l.M, b, h.DP);
                 } else {
                     dim3 grd((unsigned)(((int64_t)l.n * KC + kThreads - 1) / kThreads), S);
-                    k_dense_small<KC><<<grd, kThreads, 0, h.s>>>(l.n, chunk, l.M, b, h.DP);
+                    launch_k(k_dense_small<KC>, dim3(grd), dim3(kThreads), 0, h.s, l.n, chunk, l.M, b, h.DP);
                 }
-                k_dense_reduce<KC><<<(unsigned)(((int64_t)l.n * KC + kThreads - 1) / kThreads),
-                                     kThreads, 0, h.s>>>(l.n, S, h.DP, x);
+                launch_k(k_dense_reduce<KC>, dim3((unsigned)(((int64_t)l.n * KC + kThreads - 1) / kThreads)), dim3(kThreads), 0, h.s, l.n, S, h.DP, x);
             }
             return;
         }
@@ -1039,13 +1065,13 @@ struct Ops {
                 seg<G_ELIM>(h, l.pw, 0, l.pw.nseg, l.wcc, l.wcv, l.fn, l.fd, b, j);
                 ProfScope ps(h, "elim_restrict", j,
                              12.0 * l.w_nnz + 12.0 * l.nc + 12.0 * l.nf + Vb(2 * l.nc + l.nf));
-                k_elim_restrict<KC><<<grid_rows<KC>(l.nc), kThreads, 0, h.s>>>(
+                launch_k(k_elim_restrict<KC>, dim3(grid_rows<KC>(l.nc)), dim3(kThreads), 0, h.s, 
                     l.nc, l.cn, l.wcp, l.wcc, l.wcv, l.fn, l.fd, b, bc, hd(h, l.pw));
             }
             cycle(h, j + 1, nu1, nu2);
             ProfScope ps(h, "elim_interp", j,
                          12.0 * l.w_nnz + 24.0 * l.nf + 4.0 * l.nc + Vb(2 * l.nc + 2 * l.nf));
-            k_elim_interp<KC><<<grid_rows<KC>((int64_t)l.nc + l.nf), kThreads, 0, h.s>>>(
+            launch_k(k_elim_interp<KC>, dim3(grid_rows<KC>((int64_t)l.nc + l.nf)), dim3(kThreads), 0, h.s, 
                 l.nf, l.nc, l.cn, l.fn, l.wfp, l.wfc, l.wfv, l.fd, b, xc, x);
             return;
         }
@@ -1062,7 +1088,7 @@ struct Ops {
             seg<G_PLAIN>(h, l.pm, 0, l.pm.nseg, l.col, l.val, nullptr, nullptr, x, j);
             ProfScope ps(h, "agg_restrict", j,
                          A(l.n, l.nnz) + 4.0 * l.n + 4.0 * l.nc + Vb(2 * l.n + l.nc));
-            k_agg_restrict<KC><<<grid_rows<KC>(l.nc), kThreads, 0, h.s>>>(
+            launch_k(k_agg_restrict<KC>, dim3(grid_rows<KC>(l.nc)), dim3(kThreads), 0, h.s, 
                 l.nc, l.aptr, l.amem, l.rp, l.col, l.val, l.diag, b, x, bc, hd(h, l.pm));
         }
         cycle(h, j + 1, nu1, nu2);
@@ -1070,7 +1096,7 @@ struct Ops {
         {
             seg<G_MAPPED>(h, l.pm, 0, l.pm.nseg, l.col, l.val, l.agg, nullptr, xc, j);
             ProfScope ps(h, "agg_linesearch", j, A(l.n, l.nnz) + 4.0 * l.n + Vb(2 * l.nc));
-            k_agg_ls<KC><<<(unsigned)(pf + pc), kThreads, red_smem<KC, 1>(), h.s>>>(
+            launch_k(k_agg_ls<KC>, dim3((unsigned)(pf + pc)), dim3(kThreads), red_smem<KC, 1>(), h.s, 
                 l.n, l.nc, l.rp, l.col, l.val, l.diag, l.agg, xc, bc, h.parts, pf,
                 h.parts + pf * KC, pc, hd(h, l.pm));
         }
@@ -1078,7 +1104,7 @@ struct Ops {
         finalize<KC>(h, h.parts + pf * KC, pc, 1, 0, l.ls + KC);
         {
             ProfScope ps(h, "agg_correct", j, 4.0 * l.n + Vb(2 * l.n + l.nc));
-            k_agg_correct<KC><<<grid_rows<KC>(l.n), kThreads, 0, h.s>>>(l.n, l.agg, x, xc, l.ls);
+            launch_k(k_agg_correct<KC>, dim3(grid_rows<KC>(l.n)), dim3(kThreads), 0, h.s, l.n, l.agg, x, xc, l.ls);
         }
         for (int s = 0; s < nu2; ++s) {
             if (l.merged) jacobi(h, l, b, x);
@@ -1097,12 +1123,12 @@ struct Ops {
                          Vb(2 * cnt + (from_zero ? 0 : l.c_nbr[colr])));
         if (CF_USE_PIPE && l.contig) {
             const int64_t nrw = (cnt + kPipeRows - 1) / kPipeRows;
-            k_sweep_pipe<KC, false><<<grid_rows<KC>(nrw + (w.s_hi - w.s_lo)), kThreads, 0, h.s>>>(
+            launch_k(k_sweep_pipe<KC, false>, dim3(grid_rows<KC>(nrw + (w.s_hi - w.s_lo))), dim3(kThreads), 0, h.s, 
                 beg, cnt, nrw, l.nnz, l.rp, l.col, l.val, l.diag, b, x, nullptr,
                 from_zero ? 1 : 0, hd(h, l.pm), w);
             return;
         }
-        k_gs<KC><<<grid_rows<KC>(cnt + (w.s_hi - w.s_lo)), kThreads, 0, h.s>>>(
+        launch_k(k_gs<KC>, dim3(grid_rows<KC>(cnt + (w.s_hi - w.s_lo))), dim3(kThreads), 0, h.s, 
             l.contig ? nullptr : l.crows + beg, beg, cnt, l.rp, l.col, l.val, l.diag, b, x,
             from_zero ? 1 : 0, hd(h, l.pm), w);
     }
@@ -1119,16 +1145,15 @@ struct Ops {
             ProfScope ps(h, "jacobi_merged", lev, 12.0 * nnz + 20.0 * cnt + Vb(2 * cnt + nbr));
             if (CF_USE_PIPE && l.contig) {
                 const int64_t nrw = (cnt + kPipeRows - 1) / kPipeRows;
-                k_sweep_pipe<KC, true><<<grid_rows<KC>(nrw + (w.s_hi - w.s_lo)), kThreads, 0,
-                                         h.s>>>(beg, cnt, nrw, l.nnz, l.rp, l.col, l.val, l.diag,
+                launch_k(k_sweep_pipe<KC, true>, dim3(grid_rows<KC>(nrw + (w.s_hi - w.s_lo))), dim3(kThreads), 0, h.s, beg, cnt, nrw, l.nnz, l.rp, l.col, l.val, l.diag,
                                                 b, x, h.T, 0, hd(h, l.pm), w);
             } else
-            k_jacobi_rows<KC><<<grid_rows<KC>(cnt + (w.s_hi - w.s_lo)), kThreads, 0, h.s>>>(
+            launch_k(k_jacobi_rows<KC>, dim3(grid_rows<KC>(cnt + (w.s_hi - w.s_lo))), dim3(kThreads), 0, h.s, 
                 l.contig ? nullptr : l.crows + beg, beg, cnt, l.rp, l.col, l.val, l.diag, b, x,
                 h.T, hd(h, l.pm), w);
         }
         ProfScope ps(h, "jacobi_scatter", lev, Vb(2 * cnt) + 4.0 * cnt);
-        k_scatter_rows<KC><<<grid_rows<KC>(cnt), kThreads, 0, h.s>>>(
+        launch_k(k_scatter_rows<KC>, dim3(grid_rows<KC>(cnt)), dim3(kThreads), 0, h.s, 
             l.contig ? nullptr : l.crows + beg, beg, cnt, h.T, x);
     }
 
@@ -1180,7 +1205,7 @@ struct Ops {
         colsum(h, h.X, h.C, csum);
         {
             ProfScope ps(h, "update", 0, 3.0 * 8.0 * KC * n);
-            k_update<KC><<<grid_rows<KC>(n), kThreads, 0, h.s>>>(n, h.X, h.C, csum, h.state);
+            launch_k(k_update<KC>, dim3(grid_rows<KC>(n)), dim3(kThreads), 0, h.s, n, h.X, h.C, csum, h.state);
         }
         residual(h, h.B, h.X, h.R, h.sums);
         status(h, p, hc, use_cond);
@@ -1189,7 +1214,7 @@ struct Ops {
                        int use_cond) {
         ProfScope ps(h, "status", 0, 0.0);
         LoopCtl ctl{h.d_iter, h.d_vcyc, h.d_ncyc};
-        k_status_loop<KC><<<1, KC < 32 ? 32 : KC, 0, h.s>>>(
+        launch_k(k_status_loop<KC>, dim3(1), dim3(KC < 32 ? 32 : KC), 0, h.s, 
             h.n0, h.sums, h.bn, h.res, h.prev, h.stall, h.state, h.sums + 2 * KC, h.count,
             p.stop_margin * p.tau, p.stagnation_factor, p.stagnation_cycles, p.max_cycles, ctl, hc,
             use_cond);
@@ -1403,6 +1428,7 @@ template <int KC>
 __global__ void __launch_bounds__(kThreads) k_diag_scale(int n, const double* __restrict__ diag,
                                                          const double* __restrict__ R,
                                                          double* __restrict__ Z) {
+    CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
     int64_t i = (int64_t)blockIdx.x * Lt::RPB + slot;
     if (i >= n || !lane_ok) return;
@@ -1417,6 +1443,7 @@ __global__ void __launch_bounds__(kThreads) k_diag_scale(int n, const double* __
 template <int KC>
 __global__ void __launch_bounds__(kThreads) k_addc(int n, double* __restrict__ X,
                                                    const double* __restrict__ coef) {
+    CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
     int64_t i = (int64_t)blockIdx.x * Lt::RPB + slot;
     if (i >= n || !lane_ok) return;
@@ -1429,12 +1456,12 @@ __global__ void __launch_bounds__(kThreads) k_addc(int n, double* __restrict__ X
 template <int KC>
 void Ops<KC>::diag_scale(Hier& h, const double* Rd, double* Zd) {
     ProfScope ps(h, "fallback", 0, 0.0);
-    k_diag_scale<KC><<<grid_rows<KC>(h.n0), kThreads, 0, h.s>>>(h.n0, h.L[0].diag, Rd, Zd);
+    launch_k(k_diag_scale<KC>, dim3(grid_rows<KC>(h.n0)), dim3(kThreads), 0, h.s, h.n0, h.L[0].diag, Rd, Zd);
 }
 template <int KC>
 void Ops<KC>::k_add_const(Hier& h, double* Xd) {
     ProfScope ps(h, "addc", 0, 16.0 * KC * h.n0);
-    k_addc<KC><<<grid_rows<KC>(h.n0), kThreads, 0, h.s>>>(h.n0, Xd, h.coef);
+    launch_k(k_addc<KC>, dim3(grid_rows<KC>(h.n0)), dim3(kThreads), 0, h.s, h.n0, Xd, h.coef);
 }
 
 // ============================================================================
@@ -1451,7 +1478,7 @@ static void solve_block_t(Hier& h, int ncols, const CfSolveParams& p, double* re
         int64_t np = nparts_of(n);
         {
             ProfScope ps(h, "colstats", 0, 8.0 * KC * n);
-            k_colstats<KC><<<(unsigned)np, kThreads, red_smem<KC, 3>(), h.s>>>(n, h.B, h.parts, np);
+            launch_k(k_colstats<KC>, dim3((unsigned)np), dim3(kThreads), red_smem<KC, 3>(), h.s, n, h.B, h.parts, np);
         }
         finalize<KC>(h, h.parts, np, 3, np * KC, h.sums);
         CF_CUDA(cudaMemcpyAsync(h.h_small, h.sums, sizeof(double) * 3 * KC,
@@ -1629,12 +1656,12 @@ void solve_block(Hier& h, int kc, int ncols, const CfSolveParams& p, double* res
 void rows_to_block(Hier& h, const double* S_dev, int cnt, int kc, double* B_dev) {
     dim3 blk(32, 8), grd((h.n0 + 31) / 32, (kc + 31) / 32);
     ProfScope ps(h, "transpose", 0, 16.0 * kc * h.n0);
-    CF_DISPATCH(kc, (k_rows_to_block<K_><<<grd, blk, 0, h.s>>>(S_dev, cnt, h.n0, h.perm0, B_dev)));
+    CF_DISPATCH(kc, (launch_k(k_rows_to_block<K_>, dim3(grd), dim3(blk), 0, h.s, S_dev, cnt, h.n0, h.perm0, B_dev)));
 }
 void block_to_rows(Hier& h, const double* B_dev, int cnt, int kc, double* S_dev) {
     dim3 blk(32, 8), grd((h.n0 + 31) / 32, (kc + 31) / 32);
     ProfScope ps(h, "transpose", 0, 16.0 * kc * h.n0);
-    CF_DISPATCH(kc, (k_block_to_rows<K_><<<grd, blk, 0, h.s>>>(B_dev, cnt, h.n0, h.perm0, S_dev)));
+    CF_DISPATCH(kc, (launch_k(k_block_to_rows<K_>, dim3(grd), dim3(blk), 0, h.s, B_dev, cnt, h.n0, h.perm0, S_dev)));
 }
 void finalize_dev(Hier& h, const double* parts, int64_t nparts, int nq, int64_t qstride,
                   double* out, int kc) {
@@ -2087,11 +2114,11 @@ extern "C" int cf_solve_block_dev(void* hp, const double* B_dev, double* X_dev, 
     // B_dev is n x k row-major in node order; widen to kc columns in device order
     CF_CUDA(cudaMemsetAsync(h.B, 0, sizeof(double) * (size_t)h.n0 * kc, h.s));
     int64_t tot = (int64_t)h.n0 * k;
-    k_permute_rows<<<(unsigned)((tot + 255) / 256), 256, 0, h.s>>>(B_dev, k, h.B, kc, k, h.n0,
+    launch_k(k_permute_rows, dim3((unsigned)((tot + 255) / 256)), dim3(256), 0, h.s, B_dev, k, h.B, kc, k, h.n0,
                                                                      h.perm0, 1);
     std::vector<double> res(kc, 0.0);
     solve_block(h, kc, k, *p, res.data(), *st);
-    k_permute_rows<<<(unsigned)((tot + 255) / 256), 256, 0, h.s>>>(h.X, kc, X_dev, k, k, h.n0,
+    launch_k(k_permute_rows, dim3((unsigned)((tot + 255) / 256)), dim3(256), 0, h.s, h.X, kc, X_dev, k, k, h.n0,
                                                                      h.perm0, 0);
     CF_CUDA(cudaStreamSynchronize(h.s));
     std::memcpy(residuals, res.data(), sizeof(double) * k);
@@ -2109,10 +2136,10 @@ extern "C" int cf_residual_dev(void* hp, const double* B_dev, const double* X_de
     h.ensure_workspace(kc);
     int64_t tot = (int64_t)h.n0 * k;
     unsigned grd = (unsigned)((tot + 255) / 256);
-    k_permute_rows<<<grd, 256, 0, h.s>>>(B_dev, k, h.B, kc, k, h.n0, h.perm0, 1);
-    k_permute_rows<<<grd, 256, 0, h.s>>>(X_dev, k, h.X, kc, k, h.n0, h.perm0, 1);
+    launch_k(k_permute_rows, dim3(grd), dim3(256), 0, h.s, B_dev, k, h.B, kc, k, h.n0, h.perm0, 1);
+    launch_k(k_permute_rows, dim3(grd), dim3(256), 0, h.s, X_dev, k, h.X, kc, k, h.n0, h.perm0, 1);
     CF_DISPATCH(kc, Ops<K_>::residual(h, h.B, h.X, h.R, h.sums));
-    k_permute_rows<<<grd, 256, 0, h.s>>>(h.R, kc, R_dev, k, k, h.n0, h.perm0, 0);
+    launch_k(k_permute_rows, dim3(grd), dim3(256), 0, h.s, h.R, kc, R_dev, k, k, h.n0, h.perm0, 0);
     CF_CUDA(cudaMemcpyAsync(colsq, h.sums + k, sizeof(double) * k, cudaMemcpyDeviceToHost, h.s));
     CF_CUDA(cudaStreamSynchronize(h.s));
     CF_API_END
