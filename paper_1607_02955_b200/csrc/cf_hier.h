@@ -93,7 +93,10 @@ struct Hier {
     double* parts = nullptr;
     size_t parts_cap = 0;  // doubles
     double* SP = nullptr;  // heavy-row segment partials, max_nseg x kc_ws
-    double* fin = nullptr; // finalize stage-1 scratch
+    double* fin = nullptr; // fused-reduction segment scratch (2 regions)
+    size_t fin_region = 0;
+    unsigned* cnt = nullptr;  // fused-reduction arrival counters (2 regions + 2 globals)
+    size_t cnt_region = 0;
     double* DP = nullptr;  // dense coarse apply: per-chunk partials
     double* T = nullptr;   // merged-class Jacobi staging, max_merged x kc_ws
     int64_t max_merged = 0;
@@ -153,8 +156,8 @@ void h2d_staged(Hier& h, void* dst_dev, const void* src_host, size_t bytes);
 void d2h_staged(Hier& h, void* dst_host, const void* src_dev, size_t bytes);
 // Column sums over level-0 n x kc block -> h.sums (device), one quantity.
 void colsum_dev(Hier& h, const double* X_dev, int kc, double* out_dev);
-// out[q*kc + c] = sum_p parts[q*qstride + p*kc + c]
-void finalize_dev(Hier& h, const double* parts, int64_t nparts, int nq, int64_t qstride,
-                  double* out, int kc);
+// fused-reduction control (region 0) for kernels outside cf_solve.cu
+struct RedCtl;
+RedCtl redctl_dev(Hier& h, double* parts, int64_t np, double* out);
 
 }  // namespace cf

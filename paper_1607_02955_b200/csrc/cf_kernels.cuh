@@ -329,4 +329,63 @@ __device__ __forceinline__ void cta_reduce_store(DV<Lay<KC>::VEC> (&loc)[NQ], do
     }
 }
 
+// Fused deterministic reduction: after writing its part partial, a CTA counts
+// its arrival in its 64-part segment; the segment's last CTA sums the segment's
+// partials in part order, and the last segment finisher sums the segment sums
+// in segment order into `out` (one segment: straight into `out`).  Same
+// arithmetic as a separate two-stage finalize; no extra launches.
+constexpr int kFinSeg = 64;
+struct RedCtl {
+    double* parts = nullptr;     // [q][nparts][KC]
+    int64_t nparts = 0;
+    double* segs = nullptr;      // [q][nseg][KC] scratch
+    unsigned* seg_cnt = nullptr; // per-segment arrival counters (zero between uses)
+    unsigned* glob_cnt = nullptr;
+    double* out = nullptr;       // [q][KC]
+};
+
+template <int KC, int NQ>
+__device__ __forceinline__ void cta_reduce_finish(DV<Lay<KC>::VEC> (&loc)[NQ], double* smem,
+                                                  const RedCtl& r, int64_t part) {
+    cta_reduce_store<KC, NQ>(loc, smem, r.parts, r.nparts, part);
+    // arrival flags are broadcast with __syncthreads_or (no shared memory: the
+    // widest reductions already use the whole default 48 KB)
+    __threadfence();
+    __syncthreads();
+    const int64_t nseg = (r.nparts + kFinSeg - 1) / kFinSeg;
+    const int64_t seg = part / kFinSeg;
+    int flag = 0;
+    if (threadIdx.x == 0) {
+        const unsigned nin = (unsigned)min((int64_t)kFinSeg, r.nparts - seg * kFinSeg);
+        flag = (atomicAdd(r.seg_cnt + seg, 1u) == nin - 1);
+    }
+    if (!__syncthreads_or(flag)) return;
+    __threadfence();
+    const int64_t p0 = seg * kFinSeg, p1 = min(r.nparts, p0 + kFinSeg);
+    for (int idx = threadIdx.x; idx < NQ * KC; idx += blockDim.x) {
+        const int q = idx / KC, c = idx % KC;
+        double sum = 0.0;
+        for (int64_t p = p0; p < p1; ++p) sum += __ldcg(r.parts + ((size_t)q * r.nparts + p) * KC + c);
+        if (nseg == 1)
+            r.out[q * KC + c] = sum;
+        else
+            r.segs[((size_t)q * nseg + seg) * KC + c] = sum;
+    }
+    if (threadIdx.x == 0) r.seg_cnt[seg] = 0;
+    if (nseg == 1) return;
+    __threadfence();
+    __syncthreads();
+    flag = 0;
+    if (threadIdx.x == 0) flag = (atomicAdd(r.glob_cnt, 1u) == (unsigned)nseg - 1);
+    if (!__syncthreads_or(flag)) return;
+    __threadfence();
+    for (int idx = threadIdx.x; idx < NQ * KC; idx += blockDim.x) {
+        const int q = idx / KC, c = idx % KC;
+        double t = 0.0;
+        for (int64_t g = 0; g < nseg; ++g) t += __ldcg(r.segs + ((size_t)q * nseg + g) * KC + c);
+        r.out[q * KC + c] = t;
+    }
+    if (threadIdx.x == 0) *r.glob_cnt = 0;
+}
+
 }  // namespace cf

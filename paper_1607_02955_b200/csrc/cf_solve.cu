@@ -59,9 +59,8 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : CF_RED_CTAS)) k_res
                                                        const double* __restrict__ diag,
                                                        const double* __restrict__ B,
                                                        const double* __restrict__ X,
-                                                       double* __restrict__ R,
-                                                       double* __restrict__ parts,
-                                                       int64_t nparts, HeavyDev H) {
+                                                       double* __restrict__ R, RedCtl red,
+                                                       HeavyDev H) {
     CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
     extern __shared__ double smem[];
@@ -87,7 +86,7 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : CF_RED_CTAS)) k_res
         }
         if (R) stv<V>(R + i * KC + c0, out);
     }
-    cta_reduce_store<KC, 2>(loc, smem, parts, nparts, part);
+    cta_reduce_finish<KC, 2>(loc, smem, red, part);
 }
 
 // Y = L X (full Laplacian product) -- fallback Krylov solvers (solver.py:571-648)
@@ -115,8 +114,7 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : CF_RED_CTAS)) k_spm
 // partials of sum(b), sum|b|, sum(b^2) (balance check + norms, solver.py:672-679)
 template <int KC>
 __global__ void __launch_bounds__(kThreads) k_colstats(int n, const double* __restrict__ B,
-                                                       double* __restrict__ parts,
-                                                       int64_t nparts) {
+                                                       RedCtl red) {
     CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
     extern __shared__ double smem[];
@@ -136,7 +134,7 @@ __global__ void __launch_bounds__(kThreads) k_colstats(int n, const double* __re
             loc[2].v[t] = fma(b.v[t], b.v[t], loc[2].v[t]);
         }
     }
-    cta_reduce_store<KC, 3>(loc, smem, parts, nparts, part);
+    cta_reduce_finish<KC, 3>(loc, smem, red, part);
 }
 
 // partials of sum(U1*V1), sum(U2*V2) (fallback dot products)
@@ -145,7 +143,7 @@ __global__ void __launch_bounds__(kThreads) k_dot2(int n, const double* __restri
                                                    const double* __restrict__ V1,
                                                    const double* __restrict__ U2,
                                                    const double* __restrict__ V2,
-                                                   double* __restrict__ parts, int64_t nparts) {
+                                                   RedCtl red) {
     CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
     extern __shared__ double smem[];
@@ -164,15 +162,14 @@ __global__ void __launch_bounds__(kThreads) k_dot2(int n, const double* __restri
             loc[1].v[t] = fma(c.v[t], d.v[t], loc[1].v[t]);
         }
     }
-    cta_reduce_store<KC, 2>(loc, smem, parts, nparts, part);
+    cta_reduce_finish<KC, 2>(loc, smem, red, part);
 }
 
 // partials of column sums of X (+ Y if given, formed as fl(X+Y))
 template <int KC>
 __global__ void __launch_bounds__(kThreads) k_colsum(int n, const double* __restrict__ X,
                                                      const double* __restrict__ Y,
-                                                     double* __restrict__ parts,
-                                                     int64_t nparts) {
+                                                     RedCtl red) {
     CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
     extern __shared__ double smem[];
@@ -191,42 +188,7 @@ __global__ void __launch_bounds__(kThreads) k_colsum(int n, const double* __rest
 #pragma unroll
         for (int t = 0; t < V; ++t) loc[0].v[t] += x.v[t];
     }
-    cta_reduce_store<KC, 1>(loc, smem, parts, nparts, part);
-}
-
-// out[q*KC + c] = sum_p parts[q*qstride + p*KC + c] in a canonical order that
-// depends on nparts only: 8 contiguous segments summed left to right, then the
-// segment sums in order.
-// Canonical two-level order (depends on nparts only): segments of kFinSeg
-// consecutive parts summed left to right, then the segment sums in order.
-constexpr int kFinSeg = 64;
-// stage 1: grid (nseg, nq); out1[q][seg][KC]
-template <int KC>
-__global__ void __launch_bounds__(kThreads) k_fin1(const double* __restrict__ parts,
-                                                   int64_t nparts, int64_t qstride,
-                                                   double* __restrict__ out1, int64_t nseg) {
-    CF_PDL_ENTRY();
-    const int q = blockIdx.y;
-    const int64_t seg = blockIdx.x;
-    const double* p0 = parts + (size_t)q * qstride;
-    const int64_t beg = seg * kFinSeg, end = min(nparts, beg + kFinSeg);
-    for (int c = threadIdx.x; c < KC; c += blockDim.x) {
-        double s = 0.0;
-        for (int64_t p = beg; p < end; ++p) s += p0[p * KC + c];
-        out1[((size_t)q * nseg + seg) * KC + c] = s;
-    }
-}
-// stage 2 (or the only stage when nparts <= kFinSeg): grid nq
-template <int KC>
-__global__ void __launch_bounds__(kThreads) k_fin2(const double* __restrict__ in, int64_t cnt,
-                                                   int64_t qstride, double* __restrict__ out) {
-    CF_PDL_ENTRY();
-    const int q = blockIdx.x;
-    for (int c = threadIdx.x; c < KC; c += blockDim.x) {
-        double t = 0.0;
-        for (int64_t g = 0; g < cnt; ++g) t += in[(size_t)q * qstride + g * KC + c];
-        out[q * KC + c] = t;
-    }
+    cta_reduce_finish<KC, 1>(loc, smem, red, part);
 }
 
 // Per-column outer-iteration bookkeeping (solver.py:693-715) on the device,
@@ -616,8 +578,8 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : CF_RED_CTAS)) k_agg
     int n, int nc, const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
     const double* __restrict__ val, const double* __restrict__ diag,
     const int32_t* __restrict__ agg, const double* __restrict__ Xc,
-    const double* __restrict__ Bc, double* __restrict__ pden, int64_t pf,
-    double* __restrict__ pnum, int64_t pc, HeavyDev H) {
+    const double* __restrict__ Bc, RedCtl rden, RedCtl rnum, HeavyDev H) {
+    const int64_t pf = rden.nparts;
     CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
     extern __shared__ double smem[];
@@ -639,7 +601,7 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : CF_RED_CTAS)) k_agg
                 loc[0].v[t] = fma(d.v[t], ld, loc[0].v[t]);
             }
         }
-        cta_reduce_store<KC, 1>(loc, smem, pden, pf, part);
+        cta_reduce_finish<KC, 1>(loc, smem, rden, part);
     } else {
         const int64_t part = blockIdx.x - pf;
         for (int r = slot; r < kRowsPerPart; r += Lt::RPB) {
@@ -649,7 +611,7 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : CF_RED_CTAS)) k_agg
 #pragma unroll
             for (int t = 0; t < V; ++t) loc[0].v[t] = fma(b.v[t], x.v[t], loc[0].v[t]);
         }
-        cta_reduce_store<KC, 1>(loc, smem, pnum, pc, part);
+        cta_reduce_finish<KC, 1>(loc, smem, rnum, part);
     }
 }
 
@@ -934,19 +896,17 @@ static inline size_t red_smem() {
     return sizeof(double) * NQ * Lay<KC>::RPB * KC;
 }
 
-template <int KC>
-static void finalize(Hier& h, const double* parts, int64_t nparts, int nq, int64_t qstride,
-                     double* out) {
-    ProfScope ps(h, "finalize", -1, 8.0 * KC * nq * (nparts + 1));
-    const unsigned thr = KC < 32 ? 32 : (KC > kThreads ? kThreads : KC);
-    if (nparts <= kFinSeg) {
-        launch_k(k_fin2<KC>, dim3(nq), dim3(thr), 0, h.s, parts, nparts, qstride, out);
-    } else {
-        const int64_t nseg = (nparts + kFinSeg - 1) / kFinSeg;
-        launch_k(k_fin1<KC>, dim3(dim3((unsigned)nseg, nq)), dim3(thr), 0, h.s, parts, nparts, qstride, h.fin,
-                                                              nseg);
-        launch_k(k_fin2<KC>, dim3(nq), dim3(thr), 0, h.s, h.fin, nseg, nseg * KC, out);
-    }
+// fused-reduction control for a reduction of np parts into out; region 0/1
+// selects independent counter and scratch areas (two reductions per kernel)
+static RedCtl redctl(Hier& h, double* parts, int64_t np, double* out, int region) {
+    RedCtl r;
+    r.parts = parts;
+    r.nparts = np;
+    r.out = out;
+    r.segs = h.fin + (size_t)region * h.fin_region;
+    r.seg_cnt = h.cnt + (size_t)region * h.cnt_region;
+    r.glob_cnt = h.cnt + 2 * (size_t)h.cnt_region + region;
+    return r;
 }
 
 template <int KC>
@@ -991,25 +951,24 @@ struct Ops {
         int64_t np = nparts_of(l.n);
         seg<G_PLAIN>(h, l.pm, 0, l.pm.nseg, l.col, l.val, nullptr, nullptr, X, 0);
         ProfScope ps(h, "residual", 0, A(l.n, l.nnz) + Vb(l.n) * (R ? 3 : 2));
-        launch_k(k_residual<KC>, dim3((unsigned)np), dim3(kThreads), red_smem<KC, 2>(), h.s, 
-            l.n, l.rp, l.col, l.val, l.diag, B, X, R, h.parts, np, hd(h, l.pm));
-        finalize<KC>(h, h.parts, np, 2, np * KC, sums2);
+        launch_k(k_residual<KC>, dim3((unsigned)np), dim3(kThreads), red_smem<KC, 2>(), h.s, l.n,
+                 l.rp, l.col, l.val, l.diag, B, X, R, redctl(h, h.parts, np, sums2, 0),
+                 hd(h, l.pm));
     }
     static void colsum(Hier& h, const double* X, const double* Y, double* out) {
         int n = h.n0;
         int64_t np = nparts_of(n);
         ProfScope ps(h, "colsum", 0, Vb(n) * (Y ? 2 : 1));
-        launch_k(k_colsum<KC>, dim3((unsigned)np), dim3(kThreads), red_smem<KC, 1>(), h.s, n, X, Y, h.parts, np);
-        finalize<KC>(h, h.parts, np, 1, np * KC, out);
+        launch_k(k_colsum<KC>, dim3((unsigned)np), dim3(kThreads), red_smem<KC, 1>(), h.s, n, X, Y,
+                 redctl(h, h.parts, np, out, 0));
     }
     static void dot2(Hier& h, const double* a, const double* b, const double* c, const double* d,
                      double* out) {
         int n = h.n0;
         int64_t np = nparts_of(n);
         ProfScope ps(h, "fallback", 0, 0.0);
-        launch_k(k_dot2<KC>, dim3((unsigned)np), dim3(kThreads), red_smem<KC, 2>(), h.s, n, a, b, c, d, h.parts,
-                                                                      np);
-        finalize<KC>(h, h.parts, np, 2, np * KC, out);
+        launch_k(k_dot2<KC>, dim3((unsigned)np), dim3(kThreads), red_smem<KC, 2>(), h.s, n, a, b,
+                 c, d, redctl(h, h.parts, np, out, 0));
     }
     static void spmm(Hier& h, const double* X, double* Y) {
         DLevel& l = h.L[0];
@@ -1096,12 +1055,11 @@ struct Ops {
         {
             seg<G_MAPPED>(h, l.pm, 0, l.pm.nseg, l.col, l.val, l.agg, nullptr, xc, j);
             ProfScope ps(h, "agg_linesearch", j, A(l.n, l.nnz) + 4.0 * l.n + Vb(2 * l.nc));
-            launch_k(k_agg_ls<KC>, dim3((unsigned)(pf + pc)), dim3(kThreads), red_smem<KC, 1>(), h.s, 
-                l.n, l.nc, l.rp, l.col, l.val, l.diag, l.agg, xc, bc, h.parts, pf,
-                h.parts + pf * KC, pc, hd(h, l.pm));
+            launch_k(k_agg_ls<KC>, dim3((unsigned)(pf + pc)), dim3(kThreads), red_smem<KC, 1>(),
+                     h.s, l.n, l.nc, l.rp, l.col, l.val, l.diag, l.agg, xc, bc,
+                     redctl(h, h.parts, pf, l.ls, 0), redctl(h, h.parts + pf * KC, pc, l.ls + KC, 1),
+                     hd(h, l.pm));
         }
-        finalize<KC>(h, h.parts, pf, 1, 0, l.ls);
-        finalize<KC>(h, h.parts + pf * KC, pc, 1, 0, l.ls + KC);
         {
             ProfScope ps(h, "agg_correct", j, 4.0 * l.n + Vb(2 * l.n + l.nc));
             launch_k(k_agg_correct<KC>, dim3(grid_rows<KC>(l.n)), dim3(kThreads), 0, h.s, l.n, l.agg, x, xc, l.ls);
@@ -1478,9 +1436,9 @@ static void solve_block_t(Hier& h, int ncols, const CfSolveParams& p, double* re
         int64_t np = nparts_of(n);
         {
             ProfScope ps(h, "colstats", 0, 8.0 * KC * n);
-            launch_k(k_colstats<KC>, dim3((unsigned)np), dim3(kThreads), red_smem<KC, 3>(), h.s, n, h.B, h.parts, np);
+            launch_k(k_colstats<KC>, dim3((unsigned)np), dim3(kThreads), red_smem<KC, 3>(), h.s, n,
+                     h.B, redctl(h, h.parts, np, h.sums, 0));
         }
-        finalize<KC>(h, h.parts, np, 3, np * KC, h.sums);
         CF_CUDA(cudaMemcpyAsync(h.h_small, h.sums, sizeof(double) * 3 * KC,
                                 cudaMemcpyDeviceToHost, h.s));
         CF_CUDA(cudaStreamSynchronize(h.s));
@@ -1663,9 +1621,8 @@ void block_to_rows(Hier& h, const double* B_dev, int cnt, int kc, double* S_dev)
     ProfScope ps(h, "transpose", 0, 16.0 * kc * h.n0);
     CF_DISPATCH(kc, (launch_k(k_block_to_rows<K_>, dim3(grd), dim3(blk), 0, h.s, B_dev, cnt, h.n0, h.perm0, S_dev)));
 }
-void finalize_dev(Hier& h, const double* parts, int64_t nparts, int nq, int64_t qstride,
-                  double* out, int kc) {
-    CF_DISPATCH(kc, finalize<K_>(h, parts, nparts, nq, qstride, out));
+RedCtl redctl_dev(Hier& h, double* parts, int64_t np, double* out) {
+    return redctl(h, parts, np, out, 0);
 }
 void colsum_dev(Hier& h, const double* X_dev, int kc, double* out_dev) {
     CF_DISPATCH(kc, Ops<K_>::colsum(h, X_dev, nullptr, out_dev));
@@ -1702,6 +1659,7 @@ Hier::~Hier() {
     cudaFree(P);
     cudaFree(AP);
     cudaFree(parts);
+    cudaFree(cnt);
     cudaFree(DP);
     cudaFree(fin);
     cudaFree(SP);
@@ -1744,7 +1702,15 @@ void Hier::ensure_workspace(int kc) {
     re(parts, np * kc);
     parts_cap = np * kc;
     re(SP, (size_t)std::max<int64_t>(max_nseg, 1) * kc);
-    re(fin, (size_t)(3 * (np / kFinSeg + 2)) * kc);
+    fin_region = (size_t)(3 * (np / kFinSeg + 2)) * kc;
+    re(fin, 2 * fin_region);
+    {
+        const size_t creg = np / kFinSeg + 2;
+        if (cnt) cudaFree(cnt);
+        CF_CUDA(cudaMalloc(&cnt, sizeof(unsigned) * (2 * creg + 4)));
+        CF_CUDA(cudaMemset(cnt, 0, sizeof(unsigned) * (2 * creg + 4)));
+        cnt_region = creg;
+    }
     re(T, (size_t)std::max<int64_t>(max_merged, 1) * kc);
     {
         int64_t nd = 1;
