@@ -38,6 +38,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "multi-RHS Laplacian solves/s to ref tol; V-cycle HBM GB/s vs B200 peak"
+L2_REF_GBS = 6300 * 1.965  # full-chip L2 (LTS) throughput reference, GB/s
 
 
 def _peaks():
@@ -168,12 +169,27 @@ def cpu_reference(cfgname: str, columns: int, budget_s: float, threads: int):
             "setup_s": setup_s, "steps_timed": len(times), "s_per_step": per}
 
 
+# Bounded CPU samples per configuration (columns of the JL batch).  The
+# reference algorithm's own setup on the R-MAT graphs runs for hours (C4: 831
+# levels / 1,108 s in SURVEY.md A.2 with its stalled coarsening), so C4/C5
+# have no CPU sample.
+CPU_COLUMNS = {"c1": 64, "c2": 64, "c3": 4}
+REF_COLUMNS = {"c1": 64, "c2": 128, "c3": 8}
+CPU_UNAVAILABLE = ("reference setup on this R-MAT graph stalls into hundreds of levels "
+                   "(SURVEY.md A.2: 831 levels / 1,108 s on C4); no bounded CPU sample")
+
+
 def run_reference_arm(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return
+    if args.config not in REF_COLUMNS:
+        print(json.dumps({"impl": "reference", "metric": METRIC, "unit": "solves/s",
+                          "unavailable": CPU_UNAVAILABLE}), flush=True)
+        return
     threads = len(os.sched_getaffinity(0))
-    r = cpu_reference(args.config, args.ref_columns, args.ref_budget, threads)
+    r = cpu_reference(args.config, min(args.ref_columns, REF_COLUMNS[args.config]),
+                      args.ref_budget, threads)
     line = {"metric": METRIC, "value": r["value"], "unit": "solves/s", "n_gpus": args.gpus,
             "steps": r["steps_timed"], "warmup": 0, "ms_per_step": r["s_per_step"] * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -268,18 +284,21 @@ def run_gpu_arm(args):
     dev_h.profile(False)
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", f"profile_{args.config}_rank{rank}.txt"), "w") as f:
-        f.write("kind level launches total_ms alg_bytes GB/s\n")
-        for kind, lv, la, kms, by in sorted(rep, key=lambda r: -r[3]):
-            f.write(f"{kind} {lv} {la} {kms:.4f} {by:.0f} {by / max(kms, 1e-9) / 1e6:.1f}\n")
+        f.write("kind level launches total_ms alg_bytes alg_GB/s gather_bytes gather_GB/s\n")
+        for kind, lv, la, kms, by, gb in sorted(rep, key=lambda r: -r[3]):
+            f.write(f"{kind} {lv} {la} {kms:.4f} {by:.0f} {by / max(kms, 1e-9) / 1e6:.1f} "
+                    f"{gb:.0f} {gb / max(kms, 1e-9) / 1e6:.1f}\n")
     kinds = {}
     inst = {}
     launches = 0
-    for kind, lv, la, kms, by in rep:
+    ginst = {}
+    for kind, lv, la, kms, by, gb in rep:
         a = kinds.setdefault(kind, [0, 0.0, 0.0])
         a[0] += la
         a[1] += kms
         a[2] += by
         inst[f"{kind}@L{lv}"] = (la, kms, by)
+        ginst[f"{kind}@L{lv}"] = gb
         if kind != "memset":
             launches += la
     prof_ms = sum(v[1] for v in kinds.values())
@@ -341,8 +360,13 @@ def run_gpu_arm(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_reference(args.config, args.cpu_columns, args.cpu_budget, 1)
-        cpu = {k_: cpu[k_] for k_ in ("value", "unit", "cores", "kind", "sample")}
+        if args.config in CPU_COLUMNS:
+            cpu = cpu_reference(args.config, min(args.cpu_columns, CPU_COLUMNS[args.config]),
+                                args.cpu_budget, 1)
+            cpu = {k_: cpu[k_] for k_ in ("value", "unit", "cores", "kind", "sample")}
+        else:
+            cpu = {"value": None, "unit": "solves/s", "cores": 0, "kind": "port",
+                   "sample": "none", "unavailable": CPU_UNAVAILABLE}
 
     if rank == 0:
         line = {
@@ -358,7 +382,12 @@ def run_gpu_arm(args):
                          "frac": achieved / peak, "traffic": traffic, "kernel": dom_name,
                          "peak_source": peak_src,
                          "bytes_per_launch": dom_bytes_per_launch,
-                         "ms_per_launch": dom_ms_per_launch},
+                         "ms_per_launch": dom_ms_per_launch,
+                         "gather_bytes_per_launch": ginst[dom_name] / dom_la,
+                         "gather_gbs": ginst[dom_name] / dom_la / (dom_ms_per_launch * 1e-3) / 1e9,
+                         "l2_ref_gbs": L2_REF_GBS,
+                         "l2_ref_source": "B300_MICROARCH.md LTS cap ~6300 B/clk x 1.965 GHz "
+                                          "(B300-measured; B200 assumed similar)"},
             "step_hbm_gbs": total_bytes / (prof_ms * 1e-3) / 1e9 if prof_ms > 0 else None,
             "cpu_baseline": cpu,
             "sampling": sampling,

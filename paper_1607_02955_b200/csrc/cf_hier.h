@@ -65,7 +65,8 @@ struct DLevel {
 struct ProfRec {
     const char* kind;
     int level;
-    double bytes;
+    double bytes;   // compulsory (algorithmic) HBM bytes
+    double gbytes;  // neighbour-row gather volume (nnz * 8 * KC), served by L2/HBM
     cudaEvent_t a, b;
 };
 
@@ -119,7 +120,7 @@ struct Hier {
     std::vector<ProfRec> recs;
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
-    int prof_begin(const char* kind, int level, double bytes);
+    int prof_begin(const char* kind, int level, double bytes, double gbytes);
     void prof_end(int idx);
 
     void* stage_host = nullptr;       // pinned staging ring for pageable transfers
@@ -135,8 +136,8 @@ struct Hier {
 struct ProfScope {
     Hier& h;
     int idx = -1;
-    ProfScope(Hier& h_, const char* kind, int level, double bytes) : h(h_) {
-        if (h.prof) idx = h.prof_begin(kind, level, bytes);
+    ProfScope(Hier& h_, const char* kind, int level, double bytes, double gbytes = 0.0) : h(h_) {
+        if (h.prof) idx = h.prof_begin(kind, level, bytes, gbytes);
     }
     ~ProfScope() {
         if (idx >= 0) h.prof_end(idx);

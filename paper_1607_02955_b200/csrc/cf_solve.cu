@@ -943,14 +943,15 @@ struct Ops {
                     const double* val, const int32_t* map, const double* div, const double* X,
                     int level) {
         if (hi <= lo) return;
-        ProfScope ps(h, "heavy_seg", level, 12.0 * kSegNnz * (hi - lo) + Vb(hi - lo) * 2);
+        ProfScope ps(h, "heavy_seg", level, 12.0 * kSegNnz * (hi - lo) + Vb(hi - lo) * 2,
+                     Vb(kSegNnz * (hi - lo)));
         launch_k(k_seg<KC, MODE>, dim3((unsigned)((hi - lo + Lay<KC>::RPB - 1) / Lay<KC>::RPB)), dim3(kThreads), 0, h.s, lo, hi, pl.sbeg, pl.send, col, val, map, div, X, h.SP);
     }
     static void residual(Hier& h, const double* B, const double* X, double* R, double* sums2) {
         DLevel& l = h.L[0];
         int64_t np = nparts_of(l.n);
         seg<G_PLAIN>(h, l.pm, 0, l.pm.nseg, l.col, l.val, nullptr, nullptr, X, 0);
-        ProfScope ps(h, "residual", 0, A(l.n, l.nnz) + Vb(l.n) * (R ? 3 : 2));
+        ProfScope ps(h, "residual", 0, A(l.n, l.nnz) + Vb(l.n) * (R ? 3 : 2), Vb(l.nnz));
         launch_k(k_residual<KC>, dim3((unsigned)np), dim3(kThreads), red_smem<KC, 2>(), h.s, l.n,
                  l.rp, l.col, l.val, l.diag, B, X, R, redctl(h, h.parts, np, sums2, 0),
                  hd(h, l.pm));
@@ -1046,7 +1047,7 @@ struct Ops {
         {
             seg<G_PLAIN>(h, l.pm, 0, l.pm.nseg, l.col, l.val, nullptr, nullptr, x, j);
             ProfScope ps(h, "agg_restrict", j,
-                         A(l.n, l.nnz) + 4.0 * l.n + 4.0 * l.nc + Vb(2 * l.n + l.nc));
+                         A(l.n, l.nnz) + 4.0 * l.n + 4.0 * l.nc + Vb(2 * l.n + l.nc), Vb(l.nnz));
             launch_k(k_agg_restrict<KC>, dim3(grid_rows<KC>(l.nc)), dim3(kThreads), 0, h.s, 
                 l.nc, l.aptr, l.amem, l.rp, l.col, l.val, l.diag, b, x, bc, hd(h, l.pm));
         }
@@ -1054,7 +1055,8 @@ struct Ops {
         int64_t pf = nparts_of(l.n), pc = nparts_of(l.nc);
         {
             seg<G_MAPPED>(h, l.pm, 0, l.pm.nseg, l.col, l.val, l.agg, nullptr, xc, j);
-            ProfScope ps(h, "agg_linesearch", j, A(l.n, l.nnz) + 4.0 * l.n + Vb(2 * l.nc));
+            ProfScope ps(h, "agg_linesearch", j, A(l.n, l.nnz) + 4.0 * l.n + Vb(2 * l.nc),
+                         Vb(l.nnz));
             launch_k(k_agg_ls<KC>, dim3((unsigned)(pf + pc)), dim3(kThreads), red_smem<KC, 1>(),
                      h.s, l.n, l.nc, l.rp, l.col, l.val, l.diag, l.agg, xc, bc,
                      redctl(h, h.parts, pf, l.ls, 0), redctl(h, h.parts + pf * KC, pc, l.ls + KC, 1),
@@ -1078,7 +1080,8 @@ struct Ops {
                             from_zero ? 0 : l.pm.cseg[colr + 1]);
         ProfScope ps(h, "gs_sweep", lev,
                      12.0 * l.c_nnz[colr] + 20.0 * cnt +
-                         Vb(2 * cnt + (from_zero ? 0 : l.c_nbr[colr])));
+                         Vb(2 * cnt + (from_zero ? 0 : l.c_nbr[colr])),
+                     from_zero ? 0.0 : Vb(l.c_nnz[colr]));
         if (CF_USE_PIPE && l.contig) {
             const int64_t nrw = (cnt + kPipeRows - 1) / kPipeRows;
             launch_k(k_sweep_pipe<KC, false>, dim3(grid_rows<KC>(nrw + (w.s_hi - w.s_lo))), dim3(kThreads), 0, h.s, 
@@ -1100,7 +1103,8 @@ struct Ops {
         int64_t nnz = 0, nbr = l.merged_nbr;
         for (int c = K; c < l.ncolors; ++c) nnz += l.c_nnz[c];
         {
-            ProfScope ps(h, "jacobi_merged", lev, 12.0 * nnz + 20.0 * cnt + Vb(2 * cnt + nbr));
+            ProfScope ps(h, "jacobi_merged", lev, 12.0 * nnz + 20.0 * cnt + Vb(2 * cnt + nbr),
+                         Vb(nnz));
             if (CF_USE_PIPE && l.contig) {
                 const int64_t nrw = (cnt + kPipeRows - 1) / kPipeRows;
                 launch_k(k_sweep_pipe<KC, true>, dim3(grid_rows<KC>(nrw + (w.s_hi - w.s_lo))), dim3(kThreads), 0, h.s, beg, cnt, nrw, l.nnz, l.rp, l.col, l.val, l.diag,
@@ -1739,7 +1743,7 @@ void Hier::ensure_fallback(int kc) {
     kc_fb = kc_ws;
 }
 
-int Hier::prof_begin(const char* kind, int level, double bytes_) {
+int Hier::prof_begin(const char* kind, int level, double bytes_, double gbytes_) {
     if (ev_used + 2 > ev_pool.size()) {
         for (int t = 0; t < 64; ++t) {
             cudaEvent_t e;
@@ -1747,7 +1751,7 @@ int Hier::prof_begin(const char* kind, int level, double bytes_) {
             ev_pool.push_back(e);
         }
     }
-    ProfRec r{kind, level, bytes_, ev_pool[ev_used], ev_pool[ev_used + 1]};
+    ProfRec r{kind, level, bytes_, gbytes_, ev_pool[ev_used], ev_pool[ev_used + 1]};
     ev_used += 2;
     CF_CUDA(cudaEventRecord(r.a, s));
     recs.push_back(r);
@@ -2133,7 +2137,7 @@ extern "C" int cf_profile_report(void* hp, char* buf, int64_t cap, int64_t* need
     CF_CUDA(cudaStreamSynchronize(h.s));
     struct Agg {
         int64_t launches = 0;
-        double ms = 0, bytes = 0;
+        double ms = 0, bytes = 0, gbytes = 0;
     };
     std::map<std::pair<std::string, int>, Agg> agg;
     for (auto& r : h.recs) {
@@ -2143,12 +2147,14 @@ extern "C" int cf_profile_report(void* hp, char* buf, int64_t cap, int64_t* need
         a.launches += 1;
         a.ms += ms;
         a.bytes += r.bytes;
+        a.gbytes += r.gbytes;
     }
     std::string out;
     char line[256];
     for (auto& kv : agg) {
-        snprintf(line, sizeof line, "%s %d %lld %.6f %.1f\n", kv.first.first.c_str(),
-                 kv.first.second, (long long)kv.second.launches, kv.second.ms, kv.second.bytes);
+        snprintf(line, sizeof line, "%s %d %lld %.6f %.1f %.1f\n", kv.first.first.c_str(),
+                 kv.first.second, (long long)kv.second.launches, kv.second.ms, kv.second.bytes,
+                 kv.second.gbytes);
         out += line;
     }
     *needed = (int64_t)out.size();

@@ -373,9 +373,9 @@ class MultigridHierarchy:
     def profile(self, enable: bool) -> None:
         N.check(N.lib().cf_profile(self.device().handle, 1 if enable else 0))
 
-    def profile_report(self) -> list[tuple[str, int, int, float, float]]:
-        """[(kind, level, launches, total_ms, algorithmic_bytes)] of the launches
-        recorded since ``profile(True)``."""
+    def profile_report(self) -> list[tuple[str, int, int, float, float, float]]:
+        """[(kind, level, launches, total_ms, algorithmic_bytes, gather_bytes)] of
+        the launches recorded since ``profile(True)``."""
         need = np.zeros(1, dtype=np.int64)
         L = N.lib()
         N.check(L.cf_profile_report(self.device().handle, None, 0, N.ptr(need, N.i64p)))
@@ -384,8 +384,8 @@ class MultigridHierarchy:
                                     N.ptr(need, N.i64p)))
         out = []
         for line in buf.value.decode().splitlines():
-            k, lv, la, ms, by = line.split()
-            out.append((k, int(lv), int(la), float(ms), float(by)))
+            k, lv, la, ms, by, gb = line.split()
+            out.append((k, int(lv), int(la), float(ms), float(by), float(gb)))
         return out
 
 
