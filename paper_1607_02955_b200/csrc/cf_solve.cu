@@ -1578,17 +1578,25 @@ static void solve_block_t(Hier& h, int ncols, const CfSolveParams& p, double* re
     st.fallback_solves += fallback_cols;
 }
 
+// Chunk width for the next `rem` columns.  Measured per-width block-solve
+// cost (tools/kc_cost.py, profiles/r01/kc_cost_*.txt): 256 columns cost more
+// than two chunks of 128 (the per-level X block of 256 columns leaves the L2),
+// and widths 16..64 cost about the same as each other, so full chunks are 128
+// wide and a tail takes the smallest width that holds it.
 int pick_kc(int64_t rem) {
     static const int sizes[] = {1, 8, 16, 32, 64, 128, 256};
-    if (rem >= 32) {
-        int best = 32;
+    static const int cap = [] {
+        const char* e = std::getenv("CF_MAX_KC");
+        int c = e ? std::atoi(e) : 128;
+        int best = 1;
         for (int s : sizes)
-            if (s <= rem) best = s;
+            if (s <= c) best = s;
         return best;
-    }
+    }();
+    if (rem >= cap) return cap;
     for (int s : sizes)
         if (s >= rem) return s;
-    return 256;
+    return cap;
 }
 
 static int kc_at_least(int k) {
@@ -1797,7 +1805,22 @@ void Hier::ensure_stage() {
     for (int i = 0; i < kStagePieces; ++i) CF_CUDA(cudaEventCreateWithFlags(&stage_ev[i], cudaEventDisableTiming));
 }
 
+// Page-locked (cudaHostAlloc / cudaHostRegister) host buffers are copied by
+// DMA directly; pageable ones go through the pinned staging ring.
+static bool host_pinned(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
 void h2d_staged(Hier& h, void* dst_dev, const void* src_host, size_t bytes) {
+    if (host_pinned(src_host)) {
+        CF_CUDA(cudaMemcpyAsync(dst_dev, src_host, bytes, cudaMemcpyHostToDevice, h.s));
+        return;
+    }
     h.ensure_stage();
     size_t off = 0;
     int slot = 0;
@@ -1816,6 +1839,10 @@ void h2d_staged(Hier& h, void* dst_dev, const void* src_host, size_t bytes) {
 }
 
 void d2h_staged(Hier& h, void* dst_host, const void* src_dev, size_t bytes) {
+    if (host_pinned(dst_host)) {  // caller synchronises the stream
+        CF_CUDA(cudaMemcpyAsync(dst_host, src_dev, bytes, cudaMemcpyDeviceToHost, h.s));
+        return;
+    }
     h.ensure_stage();
     // issue up to kStagePieces DMAs ahead, drain in order
     const size_t npieces = (bytes + kStagePiece - 1) / kStagePiece;
@@ -2101,7 +2128,7 @@ extern "C" int cf_residual_dev(void* hp, const double* B_dev, const double* X_de
     Hier& h = *(Hier*)hp;
     std::lock_guard<std::mutex> lk(h.mu);
     CF_CUDA(cudaSetDevice(h.dev));
-    int kc = pick_kc(k);
+    int kc = kc_at_least(k);
     if (kc != k) throw CfError(CF_DOMAIN, "k must be a supported block width");
     h.ensure_workspace(kc);
     int64_t tot = (int64_t)h.n0 * k;

@@ -742,11 +742,16 @@ def _params(config: SolverConfig, n: int) -> N.CfSolveParams:
     return p
 
 
-def _solve_rows(hierarchy: MultigridHierarchy, rows: np.ndarray, config: SolverConfig):
+def _solve_rows(hierarchy: MultigridHierarchy, rows: np.ndarray, config: SolverConfig,
+                out: np.ndarray | None = None):
     """rows: count x n (C-contiguous fp64) -> (values count x n, residuals)."""
     n = hierarchy.n
     count = rows.shape[0]
-    out = np.empty((count, n))
+    if out is None:
+        out = np.empty((count, n))
+    elif (out.shape != (count, n) or out.dtype != np.float64
+          or not out.flags.c_contiguous or not out.flags.writeable):
+        raise DomainError(f"out must be a writeable C-contiguous float64 array of shape {(count, n)}")
     res = np.zeros(count)
     if count == 0:
         return out, res
@@ -782,15 +787,20 @@ def solve(hierarchy: MultigridHierarchy, b: Sequence[float] | np.ndarray,
 
 
 def solve_many(hierarchy: MultigridHierarchy, supplies: Sequence[Sequence[float]] | np.ndarray,
-               config: SolverConfig | None = None, threads: int = 1) -> list[PotentialVector]:
+               config: SolverConfig | None = None, threads: int = 1,
+               out: np.ndarray | None = None) -> list[PotentialVector]:
     """Solve many systems over one hierarchy (solver.py:771-811).
 
     All rows are solved together on the device; every column is computed
     independently in a fixed order, so results do not depend on ``threads``
     (accepted for API compatibility), on batch composition or on order.
+
+    ``out`` (extension, optional): a ``count x n`` float64 array that receives
+    the potentials (the returned vectors are views of its rows).  Supplies and
+    ``out`` in page-locked host memory are transferred by DMA directly.
     """
     config = config or hierarchy.config
     rows = _as_rows(hierarchy, supplies)
-    x, res = _solve_rows(hierarchy, rows, config)
+    x, res = _solve_rows(hierarchy, rows, config, out)
     return [PotentialVector(values=x[i], achieved_residual=float(res[i]))
             for i in range(rows.shape[0])]
