@@ -392,7 +392,12 @@ def run_gpu_arm(args):
                          "gather_gbs": ginst[dom_name] / dom_la / (dom_ms_per_launch * 1e-3) / 1e9,
                          "l2_ref_gbs": L2_REF_GBS,
                          "l2_ref_source": "B300_MICROARCH.md LTS cap ~6300 B/clk x 1.965 GHz "
-                                          "(B300-measured; B200 assumed similar)"},
+                                          "(B300-measured; B200 assumed similar)",
+                         # measured DRAM bytes (ncu, per launch) over the live launch time
+                         "dram_gbs": (traffic / (dom_ms_per_launch * 1e-3) / 1e9
+                                      if traffic else None),
+                         "dram_frac": (traffic / (dom_ms_per_launch * 1e-3) / 1e9 / peak
+                                       if traffic else None)},
             "step_hbm_gbs": total_bytes / (prof_ms * 1e-3) / 1e9 if prof_ms > 0 else None,
             "cpu_baseline": cpu,
             "sampling": sampling,

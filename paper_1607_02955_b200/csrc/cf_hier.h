@@ -2,6 +2,9 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <nvtx3/nvToolsExt.h>
+
+#include <cstdio>
 
 #include <map>
 #include <mutex>
@@ -14,7 +17,7 @@ namespace cf {
 // Heavy-row plan of one CSR operator (see cf_kernels.cuh): heavy rows of each
 // colour class are numbered contiguously so one class's segments form a range.
 struct Plan {
-    int64_t nheavy = 0, nseg = 0;
+    int64_t nheavy = 0, nseg = 0, heavy_nnz = 0;
     int32_t* hv = nullptr;
     int64_t* hsp = nullptr;
     int64_t* sbeg = nullptr;
@@ -52,8 +55,9 @@ struct DLevel {
     double* ls = nullptr;  // 2 x 256 line-search sums
     // per colour class (host, for the algorithmic-bytes model): rows, nnz,
     // distinct neighbour rows
-    std::vector<int64_t> c_rows, c_nnz, c_nbr;
+    std::vector<int64_t> c_rows, c_nnz, c_nbr, c_nnz_lo, c_nbr_lo;
     int64_t merged_nbr = 0;  // distinct neighbour rows of the merged Jacobi classes
+    int64_t merged_nbr_lo = 0, merged_nnz_lo = 0;
     int64_t w_nnz = 0;  // elimination: nnz(W_cf)
     int gs_classes = 0;  // colour classes swept one by one (<= kGsClasses)
     bool merged = false; // classes >= kGsClasses merged into one Jacobi step
@@ -133,14 +137,25 @@ struct Hier {
     void ensure_fallback(int kc);
 };
 
+// In profile mode each scope is also an NVTX range "cf:<kind>@L<level>", so an
+// ncu capture can select one (kind, level) instance:
+//   ncu --nvtx --nvtx-include "regex:cf:jacobi_merged@L1/" ...
 struct ProfScope {
     Hier& h;
     int idx = -1;
     ProfScope(Hier& h_, const char* kind, int level, double bytes, double gbytes = 0.0) : h(h_) {
-        if (h.prof) idx = h.prof_begin(kind, level, bytes, gbytes);
+        if (h.prof) {
+            idx = h.prof_begin(kind, level, bytes, gbytes);
+            char name[64];
+            std::snprintf(name, sizeof(name), "cf:%s@L%d", kind, level);
+            nvtxRangePushA(name);
+        }
     }
     ~ProfScope() {
-        if (idx >= 0) h.prof_end(idx);
+        if (idx >= 0) {
+            h.prof_end(idx);
+            nvtxRangePop();
+        }
     }
 };
 

@@ -85,10 +85,24 @@ struct DV {
     double v[V];
 };
 
+// Row-slice loads/stores.  A lane's V consecutive doubles are 32-byte aligned
+// when V % 4 == 0 (rows are KC * 8 bytes, KC >= 128), so one 256-bit access
+// (LDG.E.256 / STG.E.256, sm_100) moves them; a warp then reads a 1 KB row
+// with a single instruction.
+#ifndef CF_LDG256
+#define CF_LDG256 1
+#endif
 template <int V>
 __device__ __forceinline__ DV<V> ldv(const double* __restrict__ p) {
     DV<V> r;
-    if constexpr (V % 2 == 0) {
+    if constexpr (CF_LDG256 && V % 4 == 0) {
+#pragma unroll
+        for (int t = 0; t < V / 4; ++t)
+            asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                         : "=d"(r.v[4 * t]), "=d"(r.v[4 * t + 1]), "=d"(r.v[4 * t + 2]),
+                           "=d"(r.v[4 * t + 3])
+                         : "l"(p + 4 * t));
+    } else if constexpr (V % 2 == 0) {
 #pragma unroll
         for (int t = 0; t < V / 2; ++t) {
             double2 q = __ldg(reinterpret_cast<const double2*>(p) + t);
@@ -106,7 +120,15 @@ __device__ __forceinline__ DV<V> ldv(const double* __restrict__ p) {
 template <int V>
 __device__ __forceinline__ DV<V> ldv_c(const double* p) {
     DV<V> r;
-    if constexpr (V % 2 == 0) {
+    if constexpr (CF_LDG256 && V % 4 == 0) {
+#pragma unroll
+        for (int t = 0; t < V / 4; ++t)
+            asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+                         : "=d"(r.v[4 * t]), "=d"(r.v[4 * t + 1]), "=d"(r.v[4 * t + 2]),
+                           "=d"(r.v[4 * t + 3])
+                         : "l"(p + 4 * t)
+                         : "memory");
+    } else if constexpr (V % 2 == 0) {
 #pragma unroll
         for (int t = 0; t < V / 2; ++t) {
             double2 q = reinterpret_cast<const double2*>(p)[t];
@@ -122,7 +144,14 @@ __device__ __forceinline__ DV<V> ldv_c(const double* p) {
 
 template <int V>
 __device__ __forceinline__ void stv(double* p, const DV<V>& r) {
-    if constexpr (V % 2 == 0) {
+    if constexpr (CF_LDG256 && V % 4 == 0) {
+#pragma unroll
+        for (int t = 0; t < V / 4; ++t)
+            asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p + 4 * t),
+                         "d"(r.v[4 * t]), "d"(r.v[4 * t + 1]), "d"(r.v[4 * t + 2]),
+                         "d"(r.v[4 * t + 3])
+                         : "memory");
+    } else if constexpr (V % 2 == 0) {
 #pragma unroll
         for (int t = 0; t < V / 2; ++t)
             reinterpret_cast<double2*>(p)[t] = make_double2(r.v[2 * t], r.v[2 * t + 1]);
@@ -155,7 +184,8 @@ __device__ __forceinline__ void gather_row(const int32_t* __restrict__ col,
                                            int64_t end, const int32_t* __restrict__ map,
                                            const double* __restrict__ div,
                                            const double* __restrict__ X, int c0,
-                                           DV<Lay<KC>::VEC>& acc) {
+                                           DV<Lay<KC>::VEC>& acc, int jlim = 0x7fffffff) {
+    // jlim: neighbour rows j >= jlim are known to hold zero and are not read
     constexpr int V = Lay<KC>::VEC;
     constexpr int W = Lay<KC>::LPR;
     constexpr unsigned MASK = W == 32 ? 0xffffffffu : ((1u << W) - 1u);
@@ -192,7 +222,7 @@ __device__ __forceinline__ void gather_row(const int32_t* __restrict__ col,
                 int j = __shfl_sync(MASK, jj, u0 + u, W);
                 a[u] = __shfl_sync(MASK, aa, u0 + u, W);
                 if constexpr (MODE == G_ELIM) d[u] = __shfl_sync(MASK, dd, u0 + u, W);
-                if (u0 + u < cnt)
+                if (u0 + u < cnt && j < jlim)
                     x[u] = ldv<V>(X + (size_t)j * KC + c0);
                 else
                     zero(x[u]);
@@ -250,13 +280,13 @@ __device__ __forceinline__ bool seg_item(const SegWork& w, int64_t s,
                                          const int32_t* __restrict__ col,
                                          const double* __restrict__ val,
                                          const double* __restrict__ X, int c0, int& hv_out,
-                                         DV<Lay<KC>::VEC>& acc) {
+                                         DV<Lay<KC>::VEC>& acc, int jlim = 0x7fffffff) {
     constexpr int V = Lay<KC>::VEC;
     constexpr int W = Lay<KC>::LPR;
     constexpr unsigned MASK = W == 32 ? 0xffffffffu : ((1u << W) - 1u);
     const int lane = threadIdx.x & 31;
     zero(acc);
-    gather_row<KC, G_PLAIN>(col, val, w.sbeg[s], w.send[s], nullptr, nullptr, X, c0, acc);
+    gather_row<KC, G_PLAIN>(col, val, w.sbeg[s], w.send[s], nullptr, nullptr, X, c0, acc, jlim);
     stv<V>(w.SP + (size_t)s * KC + c0, acc);
     __threadfence();
     __syncwarp(MASK);

@@ -322,8 +322,8 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : kGatherCtas)) k_gs(
                                                               const double* __restrict__ diag,
                                                               const double* __restrict__ B,
                                                               double* __restrict__ X,
-                                                              int from_zero, HeavyDev H,
-                                                              SegWork w) {
+                                                              int from_zero, int jlim,
+                                                              HeavyDev H, SegWork w) {
     CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
     int64_t g = (int64_t)blockIdx.x * Lt::RPB + slot;
@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : kGatherCtas)) k_gs(
             if (H.hv && end - beg > kHeavyNnz) return;  // finished by its last segment warp
             DV<V> b = ldv<V>(B + i * KC + c0);
             const double d = diag[i];
-            gather_row<KC, G_PLAIN>(col, val, beg, end, nullptr, nullptr, X, c0, acc);
+            gather_row<KC, G_PLAIN>(col, val, beg, end, nullptr, nullptr, X, c0, acc, jlim);
 #pragma unroll
             for (int t = 0; t < V; ++t) acc.v[t] = (b.v[t] - acc.v[t]) / d;
             stv<V>(X + i * KC + c0, acc);
@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : kGatherCtas)) k_gs(
         int64_t s = w.s_lo + (g - cnt);
         if (s >= w.s_hi) return;
         int hv;
-        if (!seg_item<KC>(w, s, col, val, X, c0, hv, acc)) return;
+        if (!seg_item<KC>(w, s, col, val, X, c0, hv, acc, jlim)) return;
         i = w.h_row[hv];
     }
     DV<V> b = ldv<V>(B + i * KC + c0);
@@ -356,137 +356,6 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : kGatherCtas)) k_gs(
 #pragma unroll
     for (int t = 0; t < V; ++t) acc.v[t] = (b.v[t] - acc.v[t]) / d;
     stv<V>(X + i * KC + c0, acc);
-}
-
-// Row-pipelined smoother sweep over a contiguous row range [base, base + cnt)
-// (colour classes are contiguous in the device order).  Warp w owns rows
-// [w*kPipeRows, (w+1)*kPipeRows) of the range and, while the neighbour rows of
-// its current row are in flight, already loads the next row's row pointer,
-// first index/value chunk, b and diagonal, so a light row costs about one
-// dependent round trip.  Warps past the row warps take heavy-row segments
-// (SegWork) as in k_gs.  GS writes x in place; JACOBI writes T[q].
-constexpr int kPipeRows = 8;
-#ifndef CF_PIPE_CTAS
-#define CF_PIPE_CTAS 2
-#endif
-#ifndef CF_USE_PIPE
-#define CF_USE_PIPE 0
-#endif
-template <int KC, bool JACOBI>
-__global__ void __launch_bounds__(kThreads, CF_PIPE_CTAS)
-    k_sweep_pipe(int base, int cnt, int64_t nrw, int64_t nnz_total,
-                 const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
-                 const double* __restrict__ val, const double* __restrict__ diag,
-                 const double* __restrict__ B, double* __restrict__ X, double* __restrict__ T,
-                 int from_zero, HeavyDev H, SegWork w) {
-    CF_PDL_ENTRY();
-    CF_LANE_SETUP(KC)
-    constexpr int W = Lt::LPR;
-    constexpr unsigned MASK = W == 32 ? 0xffffffffu : ((1u << W) - 1u);
-    constexpr int G0 = CF_GATHER_DOUBLES / V;
-    constexpr int G = W < G0 ? W : G0;
-    const int64_t gw = (int64_t)blockIdx.x * Lt::RPB + slot;
-    if (!lane_ok) return;
-    if (gw >= nrw) {  // heavy-row segment warp
-        int64_t sg = w.s_lo + (gw - nrw);
-        if (sg >= w.s_hi) return;
-        DV<V> acc;
-        int hv;
-        if (!seg_item<KC>(w, sg, col, val, X, c0, hv, acc)) return;
-        const int64_t i = w.h_row[hv];
-        DV<V> b = ldv<V>(B + i * KC + c0);
-        const double d = diag[i];
-#pragma unroll
-        for (int t = 0; t < V; ++t) acc.v[t] = (b.v[t] - acc.v[t]) / d;
-        if constexpr (JACOBI)
-            stv<V>(T + (int64_t)(w.h_pos[hv] - base) * KC + c0, acc);
-        else
-            stv<V>(X + i * KC + c0, acc);
-        return;
-    }
-    const int64_t q0 = gw * kPipeRows, q1 = min((int64_t)cnt, q0 + kPipeRows);
-    if (q0 >= q1) return;
-    auto fetch = [&](int64_t p0, int& jj, double& aa) {
-        jj = 0;
-        aa = 0.0;
-        if (p0 + lane < nnz_total) {
-            jj = __ldg(col + p0 + lane);
-            aa = __ldg(val + p0 + lane);
-        }
-    };
-    int64_t i = base + q0;
-    int64_t b0 = rp[i], b1 = rp[i + 1];
-    int jj;
-    double aa;
-    fetch(b0, jj, aa);
-    DV<V> bv = ldv<V>(B + i * KC + c0);
-    double dv = diag[i];
-    for (int64_t q = q0; q < q1; ++q) {
-        i = base + q;
-        const bool has_next = q + 1 < q1;
-        // next row: metadata loads issued before this row's gathers
-        int64_t nb1 = 0;
-        int jn = 0;
-        double an = 0.0, dn = 1.0;
-        DV<V> bn;
-        zero(bn);
-        if (has_next) {
-            nb1 = rp[i + 2];
-            fetch(b1, jn, an);
-            bn = ldv<V>(B + (i + 1) * KC + c0);
-            dn = diag[i + 1];
-        }
-        const int64_t deg = b1 - b0;
-        DV<V> acc;
-        zero(acc);
-        bool write = true;
-        if (from_zero) {
-            // x = b / d (all neighbours are still zero)
-        } else if (H.hv && deg > kHeavyNnz) {
-            write = false;  // finished by its last segment warp
-        } else {
-            int64_t p0 = b0;
-            int cj = jj;
-            double ca = aa;
-            while (p0 < b1) {
-                const int cnt_c = (int)min((int64_t)W, b1 - p0);
-                for (int u0 = 0; u0 < cnt_c; u0 += G) {
-                    DV<V> x[G];
-                    double a[G];
-#pragma unroll
-                    for (int u = 0; u < G; ++u) {
-                        int j = __shfl_sync(MASK, cj, u0 + u, W);
-                        a[u] = __shfl_sync(MASK, ca, u0 + u, W);
-                        if (u0 + u < cnt_c)
-                            x[u] = ldv<V>(X + (size_t)j * KC + c0);
-                        else
-                            zero(x[u]);
-                    }
-#pragma unroll
-                    for (int u = 0; u < G; ++u)
-                        if (u0 + u < cnt_c)
-#pragma unroll
-                            for (int t = 0; t < V; ++t) acc.v[t] = fma(a[u], x[u].v[t], acc.v[t]);
-                }
-                p0 += W;
-                if (p0 < b1) fetch(p0, cj, ca);
-            }
-        }
-        if (write) {
-#pragma unroll
-            for (int t = 0; t < V; ++t) acc.v[t] = (bv.v[t] - acc.v[t]) / dv;
-            if constexpr (JACOBI)
-                stv<V>(T + q * KC + c0, acc);
-            else
-                stv<V>(X + i * KC + c0, acc);
-        }
-        b0 = b1;
-        b1 = nb1;
-        jj = jn;
-        aa = an;
-        bv = bn;
-        dv = dn;
-    }
 }
 
 // Merged trailing colour classes, one Jacobi step: T[q] = (b_i - sum_j L_ij x_j) / L_ii
@@ -497,7 +366,7 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : kGatherCtas)) k_jac
     const int32_t* __restrict__ rows, int base, int cnt, const int64_t* __restrict__ rp,
     const int32_t* __restrict__ col, const double* __restrict__ val,
     const double* __restrict__ diag, const double* __restrict__ B, const double* __restrict__ X,
-    double* __restrict__ T, HeavyDev H, SegWork w) {
+    double* __restrict__ T, int jlim, HeavyDev H, SegWork w) {
     CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
     int64_t g = (int64_t)blockIdx.x * Lt::RPB + slot;
@@ -512,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : kGatherCtas)) k_jac
         if (H.hv && end - beg > kHeavyNnz) return;
         DV<V> b = ldv<V>(B + i * KC + c0);
         const double d = diag[i];
-        gather_row<KC, G_PLAIN>(col, val, beg, end, nullptr, nullptr, X, c0, acc);
+        gather_row<KC, G_PLAIN>(col, val, beg, end, nullptr, nullptr, X, c0, acc, jlim);
 #pragma unroll
         for (int t = 0; t < V; ++t) acc.v[t] = (b.v[t] - acc.v[t]) / d;
         stv<V>(T + q * KC + c0, acc);
@@ -521,7 +390,7 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : kGatherCtas)) k_jac
     int64_t s = w.s_lo + (g - cnt);
     if (s >= w.s_hi) return;
     int hv;
-    if (!seg_item<KC>(w, s, col, val, X, c0, hv, acc)) return;
+    if (!seg_item<KC>(w, s, col, val, X, c0, hv, acc, jlim)) return;
     i = w.h_row[hv];
     q = w.h_pos[hv] - base;
     DV<V> b = ldv<V>(B + i * KC + c0);
@@ -943,15 +812,17 @@ struct Ops {
                     const double* val, const int32_t* map, const double* div, const double* X,
                     int level) {
         if (hi <= lo) return;
-        ProfScope ps(h, "heavy_seg", level, 12.0 * kSegNnz * (hi - lo) + Vb(hi - lo) * 2,
-                     Vb(kSegNnz * (hi - lo)));
+        const double hnnz = (lo == 0 && hi == pl.nseg) ? (double)pl.heavy_nnz
+                                                       : (double)kSegNnz * (hi - lo);
+        ProfScope ps(h, "heavy_seg", level, 12.0 * hnnz + Vb(hi - lo) * 2, Vb(hnnz));
         launch_k(k_seg<KC, MODE>, dim3((unsigned)((hi - lo + Lay<KC>::RPB - 1) / Lay<KC>::RPB)), dim3(kThreads), 0, h.s, lo, hi, pl.sbeg, pl.send, col, val, map, div, X, h.SP);
     }
     static void residual(Hier& h, const double* B, const double* X, double* R, double* sums2) {
         DLevel& l = h.L[0];
         int64_t np = nparts_of(l.n);
         seg<G_PLAIN>(h, l.pm, 0, l.pm.nseg, l.col, l.val, nullptr, nullptr, X, 0);
-        ProfScope ps(h, "residual", 0, A(l.n, l.nnz) + Vb(l.n) * (R ? 3 : 2), Vb(l.nnz));
+        const int64_t light = l.nnz - l.pm.heavy_nnz;  // heavy rows: the k_seg launch above
+        ProfScope ps(h, "residual", 0, A(l.n, light) + Vb(l.n) * (R ? 3 : 2), Vb(light));
         launch_k(k_residual<KC>, dim3((unsigned)np), dim3(kThreads), red_smem<KC, 2>(), h.s, l.n,
                  l.rp, l.col, l.val, l.diag, B, X, R, redctl(h, h.parts, np, sums2, 0),
                  hd(h, l.pm));
@@ -1024,7 +895,8 @@ struct Ops {
             {
                 seg<G_ELIM>(h, l.pw, 0, l.pw.nseg, l.wcc, l.wcv, l.fn, l.fd, b, j);
                 ProfScope ps(h, "elim_restrict", j,
-                             12.0 * l.w_nnz + 12.0 * l.nc + 12.0 * l.nf + Vb(2 * l.nc + l.nf));
+                             12.0 * (l.w_nnz - l.pw.heavy_nnz) + 12.0 * l.nc + 12.0 * l.nf +
+                                 Vb(2 * l.nc + l.nf));
                 launch_k(k_elim_restrict<KC>, dim3(grid_rows<KC>(l.nc)), dim3(kThreads), 0, h.s, 
                     l.nc, l.cn, l.wcp, l.wcc, l.wcv, l.fn, l.fd, b, bc, hd(h, l.pw));
             }
@@ -1035,19 +907,26 @@ struct Ops {
                 l.nf, l.nc, l.cn, l.fn, l.wfp, l.wfc, l.wfv, l.fd, b, xc, x);
             return;
         }
-        // aggregation level
-        {
+        // aggregation level.  The cycle starts from x = 0.  With contiguous
+        // colour classes the first pre-smoothing sweep reads only rows of
+        // classes it has already updated (j < first row of the class; the rest
+        // are zero), so it needs no zeroed x and writes every row.
+        const bool bounded = l.contig && nu1 > 0;
+        if (!bounded) {
             ProfScope ps(h, "memset", j, Vb(l.n));
             zero_block(h, x, (int64_t)l.n * KC);
         }
         for (int s = 0; s < nu1; ++s) {
-            for (int col = 0; col < l.gs_classes; ++col) sweep(h, l, col, b, x, s == 0 && col == 0);
-            if (l.merged) jacobi(h, l, b, x);
+            const bool first = s == 0 && bounded;
+            for (int col = 0; col < l.gs_classes; ++col)
+                sweep(h, l, col, b, x, s == 0 && col == 0, first);
+            if (l.merged) jacobi(h, l, b, x, first);
         }
         {
             seg<G_PLAIN>(h, l.pm, 0, l.pm.nseg, l.col, l.val, nullptr, nullptr, x, j);
+            const int64_t light = l.nnz - l.pm.heavy_nnz;
             ProfScope ps(h, "agg_restrict", j,
-                         A(l.n, l.nnz) + 4.0 * l.n + 4.0 * l.nc + Vb(2 * l.n + l.nc), Vb(l.nnz));
+                         A(l.n, light) + 4.0 * l.n + 4.0 * l.nc + Vb(2 * l.n + l.nc), Vb(light));
             launch_k(k_agg_restrict<KC>, dim3(grid_rows<KC>(l.nc)), dim3(kThreads), 0, h.s, 
                 l.nc, l.aptr, l.amem, l.rp, l.col, l.val, l.diag, b, x, bc, hd(h, l.pm));
         }
@@ -1055,8 +934,9 @@ struct Ops {
         int64_t pf = nparts_of(l.n), pc = nparts_of(l.nc);
         {
             seg<G_MAPPED>(h, l.pm, 0, l.pm.nseg, l.col, l.val, l.agg, nullptr, xc, j);
-            ProfScope ps(h, "agg_linesearch", j, A(l.n, l.nnz) + 4.0 * l.n + Vb(2 * l.nc),
-                         Vb(l.nnz));
+            const int64_t light = l.nnz - l.pm.heavy_nnz;
+            ProfScope ps(h, "agg_linesearch", j, A(l.n, light) + 4.0 * l.n + Vb(2 * l.nc),
+                         Vb(light));
             launch_k(k_agg_ls<KC>, dim3((unsigned)(pf + pc)), dim3(kThreads), red_smem<KC, 1>(),
                      h.s, l.n, l.nc, l.rp, l.col, l.val, l.diag, l.agg, xc, bc,
                      redctl(h, h.parts, pf, l.ls, 0), redctl(h, h.parts + pf * KC, pc, l.ls + KC, 1),
@@ -1067,52 +947,44 @@ struct Ops {
             launch_k(k_agg_correct<KC>, dim3(grid_rows<KC>(l.n)), dim3(kThreads), 0, h.s, l.n, l.agg, x, xc, l.ls);
         }
         for (int s = 0; s < nu2; ++s) {
-            if (l.merged) jacobi(h, l, b, x);
-            for (int col = l.gs_classes - 1; col >= 0; --col) sweep(h, l, col, b, x, false);
+            if (l.merged) jacobi(h, l, b, x, false);
+            for (int col = l.gs_classes - 1; col >= 0; --col) sweep(h, l, col, b, x, false, false);
         }
         (void)c;
     }
-    static void sweep(Hier& h, DLevel& l, int colr, const double* b, double* x, bool from_zero) {
+    // first: first sweep of a cycle from zero (bounded reads, see cycle())
+    static void sweep(Hier& h, DLevel& l, int colr, const double* b, double* x, bool from_zero,
+                      bool first) {
         int beg = l.cptr[colr], cnt = l.cptr[colr + 1] - beg;
         if (cnt <= 0) return;
         const int lev = (int)(&l - &h.L[0]);
         SegWork w = segwork(h, l.pm, from_zero ? 0 : l.pm.cseg[colr],
                             from_zero ? 0 : l.pm.cseg[colr + 1]);
-        ProfScope ps(h, "gs_sweep", lev,
-                     12.0 * l.c_nnz[colr] + 20.0 * cnt +
-                         Vb(2 * cnt + (from_zero ? 0 : l.c_nbr[colr])),
-                     from_zero ? 0.0 : Vb(l.c_nnz[colr]));
-        if (CF_USE_PIPE && l.contig) {
-            const int64_t nrw = (cnt + kPipeRows - 1) / kPipeRows;
-            launch_k(k_sweep_pipe<KC, false>, dim3(grid_rows<KC>(nrw + (w.s_hi - w.s_lo))), dim3(kThreads), 0, h.s, 
-                beg, cnt, nrw, l.nnz, l.rp, l.col, l.val, l.diag, b, x, nullptr,
-                from_zero ? 1 : 0, hd(h, l.pm), w);
-            return;
-        }
-        launch_k(k_gs<KC>, dim3(grid_rows<KC>(cnt + (w.s_hi - w.s_lo))), dim3(kThreads), 0, h.s, 
-            l.contig ? nullptr : l.crows + beg, beg, cnt, l.rp, l.col, l.val, l.diag, b, x,
-            from_zero ? 1 : 0, hd(h, l.pm), w);
+        const int64_t gnnz = from_zero ? 0 : first ? l.c_nnz_lo[colr] : l.c_nnz[colr];
+        const int64_t gnbr = from_zero ? 0 : first ? l.c_nbr_lo[colr] : l.c_nbr[colr];
+        ProfScope ps(h, "gs_sweep", lev, 12.0 * l.c_nnz[colr] + 20.0 * cnt + Vb(2 * cnt + gnbr),
+                     Vb(gnnz));
+        launch_k(k_gs<KC>, dim3(grid_rows<KC>(cnt + (w.s_hi - w.s_lo))), dim3(kThreads), 0, h.s,
+                 l.contig ? nullptr : l.crows + beg, beg, cnt, l.rp, l.col, l.val, l.diag, b, x,
+                 from_zero ? 1 : 0, first ? beg : 0x7fffffff, hd(h, l.pm), w);
     }
 
-    static void jacobi(Hier& h, DLevel& l, const double* b, double* x) {
+    static void jacobi(Hier& h, DLevel& l, const double* b, double* x, bool first) {
         const int K = l.gs_classes;
         int beg = l.cptr[K], cnt = l.cptr[l.ncolors] - beg;
         if (cnt <= 0) return;
         const int lev = (int)(&l - &h.L[0]);
         SegWork w = segwork(h, l.pm, l.pm.cseg[K], l.pm.cseg[l.ncolors]);
-        int64_t nnz = 0, nbr = l.merged_nbr;
+        int64_t nnz = 0;
         for (int c = K; c < l.ncolors; ++c) nnz += l.c_nnz[c];
+        const int64_t gnnz = first ? l.merged_nnz_lo : nnz;
+        const int64_t gnbr = first ? l.merged_nbr_lo : l.merged_nbr;
         {
-            ProfScope ps(h, "jacobi_merged", lev, 12.0 * nnz + 20.0 * cnt + Vb(2 * cnt + nbr),
-                         Vb(nnz));
-            if (CF_USE_PIPE && l.contig) {
-                const int64_t nrw = (cnt + kPipeRows - 1) / kPipeRows;
-                launch_k(k_sweep_pipe<KC, true>, dim3(grid_rows<KC>(nrw + (w.s_hi - w.s_lo))), dim3(kThreads), 0, h.s, beg, cnt, nrw, l.nnz, l.rp, l.col, l.val, l.diag,
-                                                b, x, h.T, 0, hd(h, l.pm), w);
-            } else
-            launch_k(k_jacobi_rows<KC>, dim3(grid_rows<KC>(cnt + (w.s_hi - w.s_lo))), dim3(kThreads), 0, h.s, 
-                l.contig ? nullptr : l.crows + beg, beg, cnt, l.rp, l.col, l.val, l.diag, b, x,
-                h.T, hd(h, l.pm), w);
+            ProfScope ps(h, "jacobi_merged", lev, 12.0 * nnz + 20.0 * cnt + Vb(2 * cnt + gnbr),
+                         Vb(gnnz));
+            launch_k(k_jacobi_rows<KC>, dim3(grid_rows<KC>(cnt + (w.s_hi - w.s_lo))), dim3(kThreads), 0, h.s,
+                     l.contig ? nullptr : l.crows + beg, beg, cnt, l.rp, l.col, l.val, l.diag, b,
+                     x, h.T, first ? beg : 0x7fffffff, hd(h, l.pm), w);
         }
         ProfScope ps(h, "jacobi_scatter", lev, Vb(2 * cnt) + 4.0 * cnt);
         launch_k(k_scatter_rows<KC>, dim3(grid_rows<KC>(cnt)), dim3(kThreads), 0, h.s, 
@@ -1900,6 +1772,7 @@ static Plan build_plan(Hier& h, int64_t n, const int64_t* rp, const int32_t* ord
             hv[i] = (int32_t)pl.nheavy;
             hrow.push_back((int32_t)i);
             hpos.push_back((int32_t)q);
+            pl.heavy_nnz += deg;
             for (int64_t b = rp[i]; b < rp[i + 1]; b += kSegNnz) {
                 sb.push_back(b);
                 se.push_back(std::min<int64_t>(b + kSegNnz, rp[i + 1]));
@@ -1983,33 +1856,44 @@ extern "C" int cf_hier_create(int32_t nlev, const CfLevelDesc* ds, int32_t devic
                 l.amem = upload(*h, d.agg_members, (size_t)d.n);
                 l.ls = (double*)h->dalloc(sizeof(double) * 2 * kMaxKC);
                 // colour-class sizes for the algorithmic-bytes model
+                // (_lo: entries / distinct rows with j below the class's first
+                // row, what the bounded first sweep reads on a contiguous level)
                 std::vector<int64_t> stamp(d.n, -1);
                 for (int c = 0; c < d.n_colors; ++c) {
                     int64_t rows = d.color_ptr[c + 1] - d.color_ptr[c], nnz = 0, nbr = 0;
+                    int64_t nnz_lo = 0, nbr_lo = 0;
                     for (int32_t q = d.color_ptr[c]; q < d.color_ptr[c + 1]; ++q) {
                         int32_t i = d.color_rows[q];
                         for (int64_t p = d.rowptr[i]; p < d.rowptr[i + 1]; ++p) {
                             ++nnz;
                             int32_t jn = d.col[p];
+                            const bool lo = jn < d.color_ptr[c];
+                            nnz_lo += lo;
                             if (stamp[jn] != c) {
                                 stamp[jn] = c;
                                 ++nbr;
+                                nbr_lo += lo;
                             }
                         }
                     }
                     l.c_rows.push_back(rows);
                     l.c_nnz.push_back(nnz);
                     l.c_nbr.push_back(nbr);
+                    l.c_nnz_lo.push_back(nnz_lo);
+                    l.c_nbr_lo.push_back(nbr_lo);
                 }
                 // distinct neighbour rows of the merged (Jacobi) classes, counted once
                 if (d.n_colors > kGsClasses) {
                     std::vector<uint8_t> seen(d.n, 0);
-                    for (int32_t q = d.color_ptr[kGsClasses]; q < d.color_ptr[d.n_colors]; ++q) {
+                    const int32_t mbeg = d.color_ptr[kGsClasses];
+                    for (int32_t q = mbeg; q < d.color_ptr[d.n_colors]; ++q) {
                         int32_t i = d.color_rows[q];
                         for (int64_t p = d.rowptr[i]; p < d.rowptr[i + 1]; ++p) {
+                            l.merged_nnz_lo += d.col[p] < mbeg;
                             if (!seen[d.col[p]]) {
                                 seen[d.col[p]] = 1;
                                 ++l.merged_nbr;
+                                l.merged_nbr_lo += d.col[p] < mbeg;
                             }
                         }
                     }

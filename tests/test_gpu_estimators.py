@@ -159,3 +159,34 @@ def test_jl_rhs_bit_exact_with_hub_nodes():
     for k in (8, 64, 200):
         ref, _ = O.jl_rhs(og, k, 5)
         assert np.array_equal(jl_rhs_rows(g, h, k, 5), ref)
+
+
+@pytest.mark.slow
+def test_config3_closeness_parity():
+    """C3 (RGG 1e6, max-degree node): JL k=128 (Q seed 0) and sampling with 256
+    pivots (seed 3) vs the reference's own values (tests/golden/config3.npz,
+    make_golden.py c3) at the config tau 1e-6 within 1e-6, and at tau_parity
+    1e-10 within 1e-8 when the fixture holds it."""
+    import os
+    from conftest import GOLDEN
+    from paper_1607_02955_b200 import configs
+    if not os.path.exists(os.path.join(GOLDEN, "config3.npz")):
+        pytest.skip("config3.npz not generated")
+    d = golden("config3.npz")
+    bc = configs.make("c3")
+    g = bc.graph
+    assert (g.n, g.m, int(bc.query[0])) == (int(d["n"]), int(d["m"]), int(d["u"]))
+    u = [int(d["u"])]
+    for tau, tag, tol in ((1e-6, "1em06", 1e-6), (1e-10, "1em10", 1e-8)):
+        if f"jl_{tag}" not in d.files:
+            continue
+        cfg = P.SolverConfig(tau=tau)
+        h = P.setup(P.laplacian(g), cfg)
+        assert h.level_sizes == d["sizes"].tolist()
+        jl = P.cf_closeness_projection(g, h, u, float(d["eps"]), 0, cfg)
+        rel = abs(jl.vector(u)[0] / d[f"jl_{tag}"][0] - 1)
+        assert rel <= tol, ("jl", tau, rel)
+        sm = P.cf_closeness_sampling(g, h, u, 256, 3, cfg)
+        rel = abs(sm.vector(u)[0] / d[f"samp_{tag}"][0] - 1)
+        assert rel <= tol, ("sampling", tau, rel)
+        assert h.stats.max_residual <= tau

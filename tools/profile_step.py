@@ -17,10 +17,14 @@ from paper_1607_02955_b200.resistance import sketch_closeness_sums  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
 ap.add_argument("--steps", type=int, default=1)
+ap.add_argument("--profile", action="store_true",
+                help="eager launches, each inside an NVTX range cf:<kind>@L<level> (ncu --nvtx)")
 args = ap.parse_args()
 bc = configs.make(args.config)
 cfg = P.SolverConfig(tau=bc.tau)
 h = P.setup(P.laplacian(bc.graph), cfg)
+if args.profile:
+    h.profile(True)
 eps = math.sqrt(math.log(bc.graph.n) / (bc.jl_k - 0.5))
 for _ in range(args.steps):
     t = time.perf_counter()
