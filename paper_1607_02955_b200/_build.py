@@ -45,19 +45,25 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, variant: str = "",
+          defines: tuple[str, ...] = ()) -> str:
+    """Build the library.  ``variant``/``defines``: an experiment build
+    ``libcfcent_b200_<variant>.so`` with extra ``-D`` macros (tuning knobs such
+    as CF_GATHER_CTAS), selected at load time with CF_LIB_VARIANT=<variant>."""
     nvcc = _nvcc()
-    os.makedirs(OBJ, exist_ok=True)
+    out = OUT if not variant else OUT.replace(".so", f"_{variant}.so")
+    obj_dir = OBJ if not variant else OBJ + "_" + variant
+    os.makedirs(obj_dir, exist_ok=True)
     jobs = []
     objs = []
     for src in SOURCES:
         path = os.path.join(CSRC, src)
         if not os.path.exists(path):
             continue
-        obj = os.path.join(OBJ, os.path.splitext(src)[0] + ".o")
+        obj = os.path.join(obj_dir, os.path.splitext(src)[0] + ".o")
         objs.append(obj)
         if force or _stale(obj, _deps(src)):
-            cmd = [nvcc, *ARCH, *NVCC_FLAGS, "-c", path, "-o", obj]
+            cmd = [nvcc, *ARCH, *NVCC_FLAGS, *("-D" + d for d in defines), "-c", path, "-o", obj]
             if src.endswith(".cu"):
                 cmd += ["-Xptxas", "-warn-spills"]
             jobs.append(cmd)
@@ -74,12 +80,16 @@ def build(verbose: bool = False, force: bool = False) -> str:
         for msg in ex.map(run, jobs):
             if verbose and msg.strip():
                 print(msg, file=sys.stderr)
-    if force or jobs or _stale(OUT, objs):
-        cmd = [nvcc, *ARCH, "-shared", "-cudart", "static", "-o", OUT, *objs, "-lpthread", "-ldl",
+    if force or jobs or _stale(out, objs):
+        cmd = [nvcc, *ARCH, "-shared", "-cudart", "static", "-o", out, *objs, "-lpthread", "-ldl",
                "-lrt"]
         run(cmd)
-    return OUT
+    return out
 
 
 if __name__ == "__main__":
-    print(build(verbose=True, force="--force" in sys.argv))
+    # python -m paper_1607_02955_b200._build [--force] [variant NAME -DMACRO=V ...]
+    args = [a for a in sys.argv[1:] if a != "--force"]
+    var = args[1] if args[:1] == ["variant"] else ""
+    defs = tuple(a[2:] for a in args if a.startswith("-D"))
+    print(build(verbose=True, force="--force" in sys.argv, variant=var, defines=defs))

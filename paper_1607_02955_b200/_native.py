@@ -16,7 +16,10 @@ import numpy as np
 from .errors import ConvergenceError, DomainError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcfcent_b200.so")
+# CF_LIB_VARIANT=<name> loads an experiment build libcfcent_b200_<name>.so
+# (_build.py ``variant``); the default is the product library.
+LIB_PATH = os.path.join(HERE, "libcfcent_b200.so" if not os.environ.get("CF_LIB_VARIANT")
+                        else f"libcfcent_b200_{os.environ['CF_LIB_VARIANT']}.so")
 
 CF_OK, CF_DOMAIN, CF_CONVERGENCE, CF_RUNTIME = 0, 1, 2, 3
 

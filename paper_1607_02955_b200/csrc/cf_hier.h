@@ -40,6 +40,11 @@ struct DLevel {
     int32_t* crows = nullptr;
     bool contig = false;  // colour classes are contiguous row ranges (crows == identity)
     int32_t *agg = nullptr, *aptr = nullptr, *amem = nullptr;
+    // aggregate pieces (restriction work items of <= kAggPiece members; an
+    // aggregate with more members is split, its pieces combined in order)
+    int64_t npieces = 0, nmulti = 0;  // pieces; pieces of split aggregates
+    int32_t *pa = nullptr, *pb = nullptr, *pslot = nullptr;
+    int* acnt = nullptr;  // split aggregate -> arrivals (zero between launches)
     int32_t *fn = nullptr, *cn = nullptr;
     double* fd = nullptr;
     int64_t* wcp = nullptr;
@@ -98,6 +103,8 @@ struct Hier {
     double* parts = nullptr;
     size_t parts_cap = 0;  // doubles
     double* SP = nullptr;  // heavy-row segment partials, max_nseg x kc_ws
+    double* PP = nullptr;  // aggregate-piece partials, max_multi x kc_ws
+    int64_t max_multi = 0;
     double* fin = nullptr; // fused-reduction segment scratch (2 regions)
     size_t fin_region = 0;
     unsigned* cnt = nullptr;  // fused-reduction arrival counters (2 regions + 2 globals)
@@ -118,6 +125,7 @@ struct Hier {
     std::map<int, cudaGraphExec_t> cycle_graphs;  // per KC
     std::map<int, cudaGraphExec_t> loop_graphs;   // whole outer iteration (while node)
     int *d_iter = nullptr, *d_ncyc = nullptr;
+    double* d_lp = nullptr;  // solve-loop parameters read by the status kernel
     long long* d_vcyc = nullptr;
     bool prof = false;
     bool host_loop = false;  // CF_HOST_LOOP=1

@@ -178,42 +178,61 @@ enum GatherMode { G_PLAIN = 0, G_MAPPED = 1, G_ELIM = 2 };
 // The working lanes of the warp load LPR consecutive (col, val) pairs with one
 // coalesced access and broadcast them by shuffle; up to 8 neighbour rows are
 // then in flight per warp.
+// A lane's share of one W-entry chunk of a CSR row: lane u < W holds entry
+// p0 + u (column, value and, for G_ELIM, the divisor), or zeros past `end`.
 template <int KC, int MODE>
-__device__ __forceinline__ void gather_row(const int32_t* __restrict__ col,
-                                           const double* __restrict__ val, int64_t beg,
-                                           int64_t end, const int32_t* __restrict__ map,
-                                           const double* __restrict__ div,
-                                           const double* __restrict__ X, int c0,
-                                           DV<Lay<KC>::VEC>& acc, int jlim = 0x7fffffff) {
+__device__ __forceinline__ void fetch_chunk(const int32_t* __restrict__ col,
+                                            const double* __restrict__ val,
+                                            const int32_t* __restrict__ map,
+                                            const double* __restrict__ div, int64_t p0,
+                                            int64_t end, int& jj, double& aa, double& dd) {
+    constexpr int W = Lay<KC>::LPR;
+    const int lane = threadIdx.x & 31;
+    jj = 0;
+    aa = 0.0;
+    dd = 1.0;
+    if (p0 + lane < end && lane < W) {
+        jj = __ldg(col + p0 + lane);
+        aa = __ldg(val + p0 + lane);
+        if constexpr (MODE == G_ELIM) dd = __ldg(div + jj);
+        if constexpr (MODE != G_PLAIN) jj = __ldg(map + jj);
+    }
+}
+
+// acc += sum_p val[p] * Y(col[p]) over p in [beg, end), ascending p (one fma
+// chain per column, identical for every block width), where
+//   G_PLAIN : Y(j) = X[j, :]
+//   G_MAPPED: Y(j) = X[map[j], :]                 (P xc gathers)
+//   G_ELIM  : Y(j) = X[map[j], :] / div[j]        (W_cf (b_f / d_f))
+// The working lanes of the warp load LPR consecutive (col, val) pairs with one
+// coalesced access and broadcast them by shuffle; up to G neighbour rows are
+// then in flight per warp.  (jj, aa, dd) is the lane's share of the first chunk
+// (fetch_chunk at beg), which a row pipeline loads one row ahead.
+template <int KC, int MODE>
+__device__ __forceinline__ void gather_row_from(const int32_t* __restrict__ col,
+                                                const double* __restrict__ val, int64_t beg,
+                                                int64_t end, const int32_t* __restrict__ map,
+                                                const double* __restrict__ div,
+                                                const double* __restrict__ X, int c0,
+                                                DV<Lay<KC>::VEC>& acc, int jj, double aa,
+                                                double dd, int jlim = 0x7fffffff) {
     // jlim: neighbour rows j >= jlim are known to hold zero and are not read
     constexpr int V = Lay<KC>::VEC;
     constexpr int W = Lay<KC>::LPR;
     constexpr unsigned MASK = W == 32 ? 0xffffffffu : ((1u << W) - 1u);
-    // rows in flight per group: 24 doubles of row data (48 registers), so the
-    // gather kernels fit 3 CTAs of 256 threads per SM
+    // rows in flight per group: CF_GATHER_DOUBLES doubles of row data per lane,
+    // so the gather kernels fit 3 CTAs of 256 threads per SM
 #ifndef CF_GATHER_DOUBLES
 #define CF_GATHER_DOUBLES 16
 #endif
     constexpr int G0 = CF_GATHER_DOUBLES / V;
     constexpr int G = W < G0 ? W : G0;
-    const int lane = threadIdx.x & 31;
-    auto fetch = [&](int64_t p0, int& jj, double& aa, double& dd) {
-        jj = 0;
-        aa = 0.0;
-        dd = 1.0;
-        if (p0 + lane < end && lane < W) {
-            jj = __ldg(col + p0 + lane);
-            aa = __ldg(val + p0 + lane);
-            if constexpr (MODE == G_ELIM) dd = __ldg(div + jj);
-            if constexpr (MODE != G_PLAIN) jj = __ldg(map + jj);
-        }
-    };
-    int jj, jn;
-    double aa, dd, an, dn;
-    fetch(beg, jj, aa, dd);
+    int jn = 0;
+    double an = 0.0, dn = 1.0;
     for (int64_t p0 = beg; p0 < end; p0 += W) {
         const int cnt = (int)min((int64_t)W, end - p0);
-        fetch(p0 + W, jn, an, dn);  // next chunk's indices overlap this chunk's row loads
+        // next chunk's indices overlap this chunk's row loads
+        if (p0 + W < end) fetch_chunk<KC, MODE>(col, val, map, div, p0 + W, end, jn, an, dn);
         for (int u0 = 0; u0 < cnt; u0 += G) {
             DV<V> x[G];
             double a[G], d[G];
@@ -243,6 +262,74 @@ __device__ __forceinline__ void gather_row(const int32_t* __restrict__ col,
         jj = jn;
         aa = an;
         dd = dn;
+    }
+}
+
+template <int KC, int MODE>
+__device__ __forceinline__ void gather_row(const int32_t* __restrict__ col,
+                                           const double* __restrict__ val, int64_t beg,
+                                           int64_t end, const int32_t* __restrict__ map,
+                                           const double* __restrict__ div,
+                                           const double* __restrict__ X, int c0,
+                                           DV<Lay<KC>::VEC>& acc, int jlim = 0x7fffffff) {
+    int jj;
+    double aa, dd;
+    fetch_chunk<KC, MODE>(col, val, map, div, beg, end, jj, aa, dd);
+    gather_row_from<KC, MODE>(col, val, beg, end, map, div, X, c0, acc, jj, aa, dd, jlim);
+}
+
+// Row pipeline: a warp visits the rows row_of(t) for t = first, first + stride,
+// ... < cnt in that order, with the next row's first index chunk and the row
+// after's row pointers in flight while the current row gathers, so a row costs
+// one exposed memory latency instead of three (row pointer -> indices ->
+// neighbour rows).  fn(t, i, beg, end, jj, aa, dd) processes row i (gathering
+// via gather_row_from with the prefetched chunk).  Per-row arithmetic is
+// unchanged; only the issue order of independent loads moves.
+template <int KC, int MODE, class RowOf, class Fn>
+__device__ __forceinline__ void row_pipeline(int64_t first, int64_t stride, int64_t cnt,
+                                             RowOf row_of, const int64_t* __restrict__ rp,
+                                             const int32_t* __restrict__ col,
+                                             const double* __restrict__ val,
+                                             const int32_t* __restrict__ map,
+                                             const double* __restrict__ div, Fn fn) {
+    int64_t t = first;
+    if (t >= cnt) return;
+    int64_t i0 = row_of(t), b0 = rp[i0], e0 = rp[i0 + 1];
+    int jj0;
+    double aa0, dd0;
+    fetch_chunk<KC, MODE>(col, val, map, div, b0, e0, jj0, aa0, dd0);
+    int64_t t1 = t + stride, i1 = 0, b1 = 0, e1 = 0;
+    if (t1 < cnt) {
+        i1 = row_of(t1);
+        b1 = rp[i1];
+        e1 = rp[i1 + 1];
+    }
+    while (true) {
+        int jj1 = 0;
+        double aa1 = 0.0, dd1 = 1.0;
+        const int64_t t2 = t1 + stride;
+        int64_t i2 = 0, b2 = 0, e2 = 0;
+        if (t1 < cnt) {
+            fetch_chunk<KC, MODE>(col, val, map, div, b1, e1, jj1, aa1, dd1);
+            if (t2 < cnt) {
+                i2 = row_of(t2);
+                b2 = rp[i2];
+                e2 = rp[i2 + 1];
+            }
+        }
+        fn(t, i0, b0, e0, jj0, aa0, dd0);
+        if (t1 >= cnt) break;
+        t = t1;
+        i0 = i1;
+        b0 = b1;
+        e0 = e1;
+        jj0 = jj1;
+        aa0 = aa1;
+        dd0 = dd1;
+        t1 = t2;
+        i1 = i2;
+        b1 = b2;
+        e1 = e2;
     }
 }
 
@@ -308,14 +395,17 @@ __device__ __forceinline__ bool seg_item(const SegWork& w, int64_t s,
     return true;
 }
 
+// Heavy rows use the partials of their segments (k_seg, summed in segment
+// order); light rows gather from the prefetched first chunk.
 template <int KC, int MODE>
-__device__ __forceinline__ void row_sum(const HeavyDev& H, int64_t i,
-                                        const int32_t* __restrict__ col,
-                                        const double* __restrict__ val, int64_t beg, int64_t end,
-                                        const int32_t* __restrict__ map,
-                                        const double* __restrict__ div,
-                                        const double* __restrict__ X, int c0,
-                                        DV<Lay<KC>::VEC>& acc) {
+__device__ __forceinline__ void row_sum_from(const HeavyDev& H, int64_t i,
+                                             const int32_t* __restrict__ col,
+                                             const double* __restrict__ val, int64_t beg,
+                                             int64_t end, const int32_t* __restrict__ map,
+                                             const double* __restrict__ div,
+                                             const double* __restrict__ X, int c0,
+                                             DV<Lay<KC>::VEC>& acc, int jj, double aa,
+                                             double dd) {
     constexpr int V = Lay<KC>::VEC;
     // heavy <=> more than kHeavyNnz entries (how the plan was built), so the
     // row-to-heavy-index lookup is only paid by heavy rows
@@ -327,9 +417,27 @@ __device__ __forceinline__ void row_sum(const HeavyDev& H, int64_t i,
             for (int t = 0; t < V; ++t) acc.v[t] += q.v[t];
         }
     } else {
-        gather_row<KC, MODE>(col, val, beg, end, map, div, X, c0, acc);
+        gather_row_from<KC, MODE>(col, val, beg, end, map, div, X, c0, acc, jj, aa, dd);
     }
 }
+
+template <int KC, int MODE>
+__device__ __forceinline__ void row_sum(const HeavyDev& H, int64_t i,
+                                        const int32_t* __restrict__ col,
+                                        const double* __restrict__ val, int64_t beg, int64_t end,
+                                        const int32_t* __restrict__ map,
+                                        const double* __restrict__ div,
+                                        const double* __restrict__ X, int c0,
+                                        DV<Lay<KC>::VEC>& acc) {
+    int jj;
+    double aa, dd;
+    fetch_chunk<KC, MODE>(col, val, map, div, beg, end, jj, aa, dd);
+    row_sum_from<KC, MODE>(H, i, col, val, beg, end, map, div, X, c0, acc, jj, aa, dd);
+}
+
+// Row kernels process tiles of kTileRows rows per CTA; warp w of the CTA takes
+// rows w, w + kWarps, ... of the tile through row_pipeline.
+constexpr int kTileRows = 64;
 
 // ---------------------------------------------------------------------------
 // CTA-level deterministic column reduction: every thread holds NQ partial

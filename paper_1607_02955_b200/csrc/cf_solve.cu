@@ -68,23 +68,28 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : CF_RED_CTAS)) k_res
     zero(loc[0]);
     zero(loc[1]);
     const int64_t part = blockIdx.x;
-    for (int r = slot; r < kRowsPerPart; r += Lt::RPB) {
-        int64_t i = part * kRowsPerPart + r;
-        if (i >= n || !lane_ok) break;
-        DV<V> acc;
-        zero(acc);
-        row_sum<KC, G_PLAIN>(H, i, col, val, rp[i], rp[i + 1], nullptr, nullptr, X, c0, acc);
-        DV<V> b = ldv<V>(B + i * KC + c0), x = ldv<V>(X + i * KC + c0);
-        double d = diag[i];
-        DV<V> out;
+    if (lane_ok) {
+        const int64_t r0 = part * kRowsPerPart;
+        row_pipeline<KC, G_PLAIN>(
+            r0 + slot, Lt::RPB, min((int64_t)n, r0 + kRowsPerPart), [](int64_t t) { return t; },
+            rp, col, val, nullptr, nullptr,
+            [&](int64_t, int64_t i, int64_t beg, int64_t end, int jj, double aa, double dd) {
+                DV<V> acc;
+                zero(acc);
+                row_sum_from<KC, G_PLAIN>(H, i, col, val, beg, end, nullptr, nullptr, X, c0, acc,
+                                          jj, aa, dd);
+                DV<V> b = ldv<V>(B + i * KC + c0), x = ldv<V>(X + i * KC + c0);
+                const double d = diag[i];
+                DV<V> out;
 #pragma unroll
-        for (int t = 0; t < V; ++t) {
-            double v = b.v[t] - fma(d, x.v[t], acc.v[t]);
-            out.v[t] = v;
-            loc[0].v[t] += v;
-            loc[1].v[t] = fma(v, v, loc[1].v[t]);
-        }
-        if (R) stv<V>(R + i * KC + c0, out);
+                for (int t = 0; t < V; ++t) {
+                    double v = b.v[t] - fma(d, x.v[t], acc.v[t]);
+                    out.v[t] = v;
+                    loc[0].v[t] += v;
+                    loc[1].v[t] = fma(v, v, loc[1].v[t]);
+                }
+                if (R) stv<V>(R + i * KC + c0, out);
+            });
     }
     cta_reduce_finish<KC, 2>(loc, smem, red, part);
 }
@@ -197,6 +202,7 @@ __global__ void __launch_bounds__(kThreads) k_colsum(int n, const double* __rest
 // graph.  Check c (0-based) is a regular check for c < max_cycles and the
 // reference's loop-exhausted final check for c == max_cycles.
 struct LoopCtl {
+    const double* lp;        // stop, stagnation factor, stagnation cycles, max cycles
     int* iter;               // checks done
     long long* vcyc;         // column V-cycles executed
     int* ncyc;               // block V-cycles executed
@@ -206,10 +212,13 @@ __global__ void k_status_loop(int n, const double* __restrict__ sums,
                               const double* __restrict__ bn, double* __restrict__ res,
                               double* __restrict__ prev, int* __restrict__ stall,
                               int* __restrict__ state, double* __restrict__ mean,
-                              int* __restrict__ count, double stop, double sfac, int scyc,
-                              int max_cycles, LoopCtl ctl, cudaGraphConditionalHandle cond,
-                              int use_cond) {
+                              int* __restrict__ count, LoopCtl ctl,
+                              cudaGraphConditionalHandle cond, int use_cond) {
     CF_PDL_ENTRY();
+    // loop parameters live in device memory so a captured solve graph serves
+    // every tolerance (they are not baked into the graph)
+    const double stop = ctl.lp[0], sfac = ctl.lp[1];
+    const int scyc = (int)ctl.lp[2], max_cycles = (int)ctl.lp[3];
     const int c = threadIdx.x;
     const int check = *ctl.iter;
     const bool final_check = check >= max_cycles;
@@ -414,20 +423,32 @@ __global__ void __launch_bounds__(kThreads) k_scatter_rows(const int32_t* __rest
 }
 
 // bc[a] = sum_{i in a} (b_i - L_i x)  (residual fused with P^T, solver.py:548-549)
+// One warp per aggregate piece: pieces are runs of at most kAggPiece members of
+// one aggregate (kAggPiece = the reference's aggregate cap, so reference-cap
+// hierarchies have one piece per aggregate and a single member chain).  A
+// split aggregate's pieces write partials to PP; the last-arriving piece sums
+// them in piece order (fixed order, independent of scheduling).
+constexpr int kAggPiece = 8;
 template <int KC>
 __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : CF_RED_CTAS)) k_agg_restrict(
-    int nc, const int32_t* __restrict__ aptr, const int32_t* __restrict__ amem,
+    int64_t np, const int32_t* __restrict__ pa, const int32_t* __restrict__ pb,
+    const int32_t* __restrict__ pslot, int* __restrict__ acnt, double* __restrict__ PP,
+    const int32_t* __restrict__ aptr, const int32_t* __restrict__ amem,
     const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
     const double* __restrict__ val, const double* __restrict__ diag,
     const double* __restrict__ B, const double* __restrict__ X, double* __restrict__ Bc,
     HeavyDev H) {
     CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
-    int64_t a = (int64_t)blockIdx.x * Lt::RPB + slot;
-    if (a >= nc || !lane_ok) return;
+    const int64_t p = (int64_t)blockIdx.x * Lt::RPB + slot;
+    if (p >= np || !lane_ok) return;
+    const int64_t a = pa ? pa[p] : p;
+    const int a0 = aptr[a], a1 = aptr[a + 1];
+    const int q0 = pb ? pb[p] : a0;
+    const int q1 = pb ? min(a1, q0 + kAggPiece) : a1;
     DV<V> out;
     zero(out);
-    for (int q = aptr[a]; q < aptr[a + 1]; ++q) {
+    for (int q = q0; q < q1; ++q) {
         int64_t i = amem[q];
         DV<V> acc;
         zero(acc);
@@ -437,6 +458,30 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : CF_RED_CTAS)) k_agg
 #pragma unroll
         for (int t = 0; t < V; ++t) out.v[t] += b.v[t] - fma(d, x.v[t], acc.v[t]);
     }
+    if (q0 == a0 && q1 == a1) {
+        stv<V>(Bc + a * KC + c0, out);
+        return;
+    }
+    // split aggregate
+    const int ps = pslot[p];
+    constexpr unsigned MASK = Lt::LPR == 32 ? 0xffffffffu : ((1u << Lt::LPR) - 1u);
+    stv<V>(PP + (size_t)ps * KC + c0, out);
+    __threadfence();
+    __syncwarp(MASK);
+    const int npc = (a1 - a0 + kAggPiece - 1) / kAggPiece;
+    int old = 0;
+    if ((threadIdx.x & 31) == 0) old = atomicAdd(acnt + a, 1);
+    old = __shfl_sync(MASK, old, 0);
+    if (old != npc - 1) return;
+    __threadfence();
+    const int first = ps - (q0 - a0) / kAggPiece;
+    zero(out);
+    for (int k = 0; k < npc; ++k) {
+        const double* q = PP + (size_t)(first + k) * KC + c0;
+#pragma unroll
+        for (int t = 0; t < V; ++t) out.v[t] += __ldcg(q + t);
+    }
+    if ((threadIdx.x & 31) == 0) acnt[a] = 0;
     stv<V>(Bc + a * KC + c0, out);
 }
 
@@ -552,27 +597,36 @@ __global__ void __launch_bounds__(kThreads, 2) k_elim_interp(
     int nf, int nc, const int32_t* __restrict__ cn, const int32_t* __restrict__ fn,
     const int64_t* __restrict__ wp, const int32_t* __restrict__ wc,
     const double* __restrict__ wv, const double* __restrict__ fd,
-    const double* __restrict__ B, const double* __restrict__ Xc, double* __restrict__ X) {
+    const double* __restrict__ B, const double* __restrict__ Xc, double* __restrict__ X,
+    int rpw) {
     CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
-    int64_t g = (int64_t)blockIdx.x * Lt::RPB + slot;
     if (!lane_ok) return;
-    if (g < nc) {
-        DV<V> x = ldv<V>(Xc + g * KC + c0);
-        stv<V>(X + (size_t)cn[g] * KC + c0, x);
+    const int64_t tile = (int64_t)Lt::RPB * rpw;
+    const int64_t ctile = ((int64_t)nc + tile - 1) / tile;
+    if ((int64_t)blockIdx.x < ctile) {
+        const int64_t g0 = (int64_t)blockIdx.x * tile;
+        const int64_t gend = min((int64_t)nc, g0 + tile);
+        for (int64_t g = g0 + slot; g < gend; g += Lt::RPB)
+            stv<V>(X + (size_t)cn[g] * KC + c0, ldv<V>(Xc + g * KC + c0));
         return;
     }
-    g -= nc;
-    if (g >= nf) return;
-    DV<V> acc;
-    zero(acc);
-    gather_row<KC, G_PLAIN>(wc, wv, wp[g], wp[g + 1], nullptr, nullptr, Xc, c0, acc);
-    int64_t i = fn[g];
-    DV<V> b = ldv<V>(B + i * KC + c0);
-    double d = fd[g];
+    const int64_t r0 = ((int64_t)blockIdx.x - ctile) * tile;
+    row_pipeline<KC, G_PLAIN>(
+        r0 + slot, Lt::RPB, min((int64_t)nf, r0 + tile), [](int64_t t) { return t; }, wp, wc,
+        wv, nullptr, nullptr,
+        [&](int64_t g, int64_t, int64_t beg, int64_t end, int jj, double aa, double dd) {
+            DV<V> acc;
+            zero(acc);
+            gather_row_from<KC, G_PLAIN>(wc, wv, beg, end, nullptr, nullptr, Xc, c0, acc, jj, aa,
+                                         dd);
+            const int64_t i = fn[g];
+            DV<V> b = ldv<V>(B + i * KC + c0);
+            const double d = fd[g];
 #pragma unroll
-    for (int t = 0; t < V; ++t) acc.v[t] = (b.v[t] + acc.v[t]) / d;
-    stv<V>(X + i * KC + c0, acc);
+            for (int t = 0; t < V; ++t) acc.v[t] = (b.v[t] + acc.v[t]) / d;
+            stv<V>(X + i * KC + c0, acc);
+        });
 }
 
 // coarsest: x = M b, M dense n x n (solver.py:406-419 restated as one operator).
@@ -757,8 +811,24 @@ __global__ void k_permute_rows(const double* __restrict__ src, int ks, double* _
 
 static inline int64_t nparts_of(int64_t n) { return (n + kRowsPerPart - 1) / kRowsPerPart; }
 template <int KC>
-static inline unsigned grid_rows(int64_t rows) {
-    return (unsigned)std::max<int64_t>(1, (rows + Lay<KC>::RPB - 1) / Lay<KC>::RPB);
+static inline unsigned grid_rows(int64_t rows, int64_t at_least = 1) {
+    return (unsigned)std::max<int64_t>(at_least, (rows + Lay<KC>::RPB - 1) / Lay<KC>::RPB);
+}
+static inline unsigned grid_tiles(int64_t rows, int64_t at_least = 1, int rpw = kTileRows / kWarps) {
+    const int64_t t = (int64_t)kWarps * rpw;
+    return (unsigned)std::max<int64_t>(at_least, (rows + t - 1) / t);
+}
+// Rows per warp of the tiled row kernels: the row pipeline pays off with
+// several rows per warp, but a launch must still fill the GPU several waves
+// deep (148 SMs x 3 CTAs x kWaves), or small levels lose parallelism.
+#ifndef CF_RPW_MAX
+#define CF_RPW_MAX 8
+#endif
+static inline int pick_rpw(int64_t rows) {
+    constexpr int64_t kSlots = 148 * 3 * kWarps, kWaves = 4;
+    int r = CF_RPW_MAX;
+    while (r > 1 && rows < kSlots * kWaves * r) r >>= 1;
+    return r;
 }
 template <int KC, int NQ>
 static inline size_t red_smem() {
@@ -897,14 +967,17 @@ struct Ops {
                 ProfScope ps(h, "elim_restrict", j,
                              12.0 * (l.w_nnz - l.pw.heavy_nnz) + 12.0 * l.nc + 12.0 * l.nf +
                                  Vb(2 * l.nc + l.nf));
-                launch_k(k_elim_restrict<KC>, dim3(grid_rows<KC>(l.nc)), dim3(kThreads), 0, h.s, 
-                    l.nc, l.cn, l.wcp, l.wcc, l.wcv, l.fn, l.fd, b, bc, hd(h, l.pw));
+                launch_k(k_elim_restrict<KC>, dim3(grid_rows<KC>(l.nc)), dim3(kThreads), 0, h.s,
+                         l.nc, l.cn, l.wcp, l.wcc, l.wcv, l.fn, l.fd, b, bc, hd(h, l.pw));
             }
             cycle(h, j + 1, nu1, nu2);
             ProfScope ps(h, "elim_interp", j,
                          12.0 * l.w_nnz + 24.0 * l.nf + 4.0 * l.nc + Vb(2 * l.nc + 2 * l.nf));
-            launch_k(k_elim_interp<KC>, dim3(grid_rows<KC>((int64_t)l.nc + l.nf)), dim3(kThreads), 0, h.s, 
-                l.nf, l.nc, l.cn, l.fn, l.wfp, l.wfc, l.wfv, l.fd, b, xc, x);
+            const int rpw = pick_rpw(l.nf);
+            launch_k(k_elim_interp<KC>,
+                     dim3(std::max(1u, grid_tiles(l.nc, 0, rpw) + grid_tiles(l.nf, 0, rpw))),
+                     dim3(kThreads), 0, h.s, l.nf, l.nc, l.cn, l.fn, l.wfp, l.wfc, l.wfv, l.fd, b,
+                     xc, x, rpw);
             return;
         }
         // aggregation level.  The cycle starts from x = 0.  With contiguous
@@ -927,8 +1000,9 @@ struct Ops {
             const int64_t light = l.nnz - l.pm.heavy_nnz;
             ProfScope ps(h, "agg_restrict", j,
                          A(l.n, light) + 4.0 * l.n + 4.0 * l.nc + Vb(2 * l.n + l.nc), Vb(light));
-            launch_k(k_agg_restrict<KC>, dim3(grid_rows<KC>(l.nc)), dim3(kThreads), 0, h.s, 
-                l.nc, l.aptr, l.amem, l.rp, l.col, l.val, l.diag, b, x, bc, hd(h, l.pm));
+            launch_k(k_agg_restrict<KC>, dim3(grid_rows<KC>(l.npieces)), dim3(kThreads), 0, h.s,
+                     (int64_t)l.npieces, l.pa, l.pb, l.pslot, l.acnt, h.PP, l.aptr, l.amem,
+                     l.rp, l.col, l.val, l.diag, b, x, bc, hd(h, l.pm));
         }
         cycle(h, j + 1, nu1, nu2);
         int64_t pf = nparts_of(l.n), pc = nparts_of(l.nc);
@@ -1047,10 +1121,9 @@ struct Ops {
     static void status(Hier& h, const CfSolveParams& p, cudaGraphConditionalHandle hc,
                        int use_cond) {
         ProfScope ps(h, "status", 0, 0.0);
-        LoopCtl ctl{h.d_iter, h.d_vcyc, h.d_ncyc};
+        LoopCtl ctl{h.d_lp, h.d_iter, h.d_vcyc, h.d_ncyc};
         launch_k(k_status_loop<KC>, dim3(1), dim3(KC < 32 ? 32 : KC), 0, h.s, 
-            h.n0, h.sums, h.bn, h.res, h.prev, h.stall, h.state, h.sums + 2 * KC, h.count,
-            p.stop_margin * p.tau, p.stagnation_factor, p.stagnation_cycles, p.max_cycles, ctl, hc,
+            h.n0, h.sums, h.bn, h.res, h.prev, h.stall, h.state, h.sums + 2 * KC, h.count, ctl, hc,
             use_cond);
     }
 
@@ -1356,6 +1429,9 @@ static void solve_block_t(Hier& h, int ncols, const CfSolveParams& p, double* re
     int64_t fallback_cols = 0;
     if (nactive > 0) {
         // check 0 on the host path, then the device-controlled loop
+        const double lp[4] = {stop, p.stagnation_factor, (double)p.stagnation_cycles,
+                              (double)p.max_cycles};
+        CF_CUDA(cudaMemcpyAsync(h.d_lp, lp, sizeof lp, cudaMemcpyHostToDevice, h.s));
         CF_CUDA(cudaMemsetAsync(h.d_iter, 0, sizeof(int), h.s));
         CF_CUDA(cudaMemsetAsync(h.d_vcyc, 0, sizeof(long long), h.s));
         CF_CUDA(cudaMemsetAsync(h.d_ncyc, 0, sizeof(int), h.s));
@@ -1586,6 +1662,7 @@ void Hier::ensure_workspace(int kc) {
     re(parts, np * kc);
     parts_cap = np * kc;
     re(SP, (size_t)std::max<int64_t>(max_nseg, 1) * kc);
+    re(PP, (size_t)std::max<int64_t>(max_multi, 1) * kc);
     fin_region = (size_t)(3 * (np / kFinSeg + 2)) * kc;
     re(fin, 2 * fin_region);
     {
@@ -1854,6 +1931,35 @@ extern "C" int cf_hier_create(int32_t nlev, const CfLevelDesc* ds, int32_t devic
                 l.agg = upload(*h, d.agg, (size_t)d.n);
                 l.aptr = upload(*h, d.agg_ptr, (size_t)d.n_coarse + 1);
                 l.amem = upload(*h, d.agg_members, (size_t)d.n);
+                {
+                    // restriction pieces: only when some aggregate exceeds kAggPiece
+                    std::vector<int32_t> pa, pb, pslot;
+                    bool split = false;
+                    for (int32_t a = 0; a < d.n_coarse && !split; ++a)
+                        split = d.agg_ptr[a + 1] - d.agg_ptr[a] > kAggPiece;
+                    if (split) {
+                        int32_t nm = 0;
+                        for (int32_t a = 0; a < d.n_coarse; ++a) {
+                            const int32_t a0 = d.agg_ptr[a], a1 = d.agg_ptr[a + 1];
+                            const bool multi = a1 - a0 > kAggPiece;
+                            for (int32_t q = a0; q < a1 || q == a0; q += kAggPiece) {
+                                pa.push_back(a);
+                                pb.push_back(q);
+                                pslot.push_back(multi ? nm++ : -1);
+                            }
+                        }
+                        l.npieces = (int64_t)pa.size();
+                        l.nmulti = nm;
+                        l.pa = upload(*h, pa.data(), pa.size());
+                        l.pb = upload(*h, pb.data(), pb.size());
+                        l.pslot = upload(*h, pslot.data(), pslot.size());
+                        l.acnt = (int*)h->dalloc(sizeof(int) * (size_t)std::max(d.n_coarse, 1));
+                        CF_CUDA(cudaMemset(l.acnt, 0, sizeof(int) * (size_t)std::max(d.n_coarse, 1)));
+                        h->max_multi = std::max<int64_t>(h->max_multi, nm);
+                    } else {
+                        l.npieces = d.n_coarse;
+                    }
+                }
                 l.ls = (double*)h->dalloc(sizeof(double) * 2 * kMaxKC);
                 // colour-class sizes for the algorithmic-bytes model
                 // (_lo: entries / distinct rows with j below the class's first
@@ -1931,6 +2037,7 @@ extern "C" int cf_hier_create(int32_t nlev, const CfLevelDesc* ds, int32_t devic
         // cannot attribute kernels inside graphs with conditional nodes)
         if (const char* e = std::getenv("CF_HOST_LOOP")) h->host_loop = std::atoi(e) != 0;
         h->d_iter = (int*)h->dalloc(sizeof(int) * 4);
+        h->d_lp = (double*)h->dalloc(sizeof(double) * 4);
         h->d_ncyc = (int*)h->dalloc(sizeof(int) * 4);
         h->d_vcyc = (long long*)h->dalloc(sizeof(long long) * 2);
         CF_CUDA(cudaMallocHost(&h->h_count, sizeof(int) * 4));

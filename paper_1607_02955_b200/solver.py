@@ -25,6 +25,7 @@ updated in parallel.  Every other V-cycle step is the reference's.
 
 from __future__ import annotations
 
+import os
 import threading
 from dataclasses import dataclass, field
 from enum import Enum
@@ -79,6 +80,14 @@ STALL_FILL_FACTOR = 2.0                 # min(sum d_f^2, |C|^2) <= factor * nnz
 STALL_AGG_CAP = 64
 STALL_AGG_THRESHOLD = 0.0
 STALL_BREAKER_MIN_N0 = 262144
+# Hub levels (B200 setup): on levels of a large graph (n0 >
+# STALL_BREAKER_MIN_N0) whose maximum off-degree exceeds HUB_DEGREE_RATIO x the
+# mean, the reference's aggregate cap of 8 leaves a hub's edges to its many
+# small aggregates in the Galerkin operator (R-MAT: coarse levels with mean
+# degree 90-280 and as many nonzeros as the fine level).  There the aggregate
+# cap is HUB_AGG_CAP.  Geometric graphs (C3: max/mean 2.9) never qualify.
+HUB_DEGREE_RATIO = 64.0
+HUB_AGG_CAP = int(os.environ.get("CF_HUB_AGG_CAP", "512"))
 
 
 @dataclass(frozen=True)
@@ -646,6 +655,11 @@ def setup(matrix: sp.spmatrix, config: SolverConfig | None = None,
         if stall_breaker is not None:
             return bool(stall_breaker)
         return n0 > STALL_BREAKER_MIN_N0 or n_level > DEVICE_DIRECT_MAX
+    def hub_level(mat) -> bool:
+        if stall_breaker is False or n0 <= STALL_BREAKER_MIN_N0:
+            return False
+        offdeg = np.diff(mat.indptr) - 1
+        return offdeg.max() > HUB_DEGREE_RATIO * max(offdeg.mean(), 1.0)
     while current.shape[0] > config.max_direct_size:
         n_cur = current.shape[0]
         need = MIN_REDUCTION * n_cur
@@ -659,7 +673,8 @@ def setup(matrix: sp.spmatrix, config: SolverConfig | None = None,
                 else:
                     vec = relaxed_test_vectors(current, config.aggregation_test_vectors, rng)
                     tvecs[n_cur] = vec
-                    coarse, agg = coarsen_aggregate(current, vec)
+                    cap = HUB_AGG_CAP if hub_level(current) else MAX_AGGREGATE_SIZE
+                    coarse, agg = coarsen_aggregate(current, vec, cap)
                     red = n_cur - (int(agg.max()) + 1)
                     if red < need:
                         mc, ma = _matching_aggregation(current, vec)

@@ -201,6 +201,10 @@ def config3(tau_list=(1e-6, 1e-10)):
     u = int(np.argmax(deg))
     eps = math.sqrt(math.log(g.n) / 127.5)
     d = {"n": np.int64(g.n), "m": np.int64(g.m), "u": np.int64(u), "eps": np.float64(eps)}
+    old = os.path.join(OUT, "config3.npz")
+    if os.path.exists(old):  # keep values of earlier runs (one tau per run is hours)
+        with np.load(old, allow_pickle=True) as prev:
+            d.update({k: prev[k] for k in prev.files if k != "provenance"})
     for tau in tau_list:
         cfg = slv.SolverConfig(tau=tau, seed=0)
         t0 = time.perf_counter()
@@ -233,3 +237,5 @@ if __name__ == "__main__":
         config2()
     if "c3" in which:
         config3()
+    if "c3tau10" in which:  # the tau_parity values alone (~2 h of reference CPU time)
+        config3((1e-10,))

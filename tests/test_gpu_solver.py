@@ -203,3 +203,43 @@ def test_config4_properties():
     for pot, b_ in zip(P.solve_many(h, s, cfg), s):
         assert np.linalg.norm(b_ - lap @ pot.values) / np.linalg.norm(b_) <= bc.tau
     assert h.stats.fallback_solves == 0
+
+
+def test_split_aggregates(rng, monkeypatch):
+    """Aggregates larger than the restriction piece (8 members; hub levels of
+    power-law graphs use cap 64) are restricted in pieces combined in a fixed
+    order: solutions match the dense oracle and stay bitwise independent of the
+    block width."""
+    from paper_1607_02955_b200 import solver as S
+    monkeypatch.setattr(S, "MAX_AGGREGATE_SIZE", 64)
+    g = G.barabasi_albert_graph(6000, 2, 7)
+    lap = P.laplacian(g)
+    h = P.setup(lap, P.SolverConfig(tau=1e-10))
+    big = [int(np.bincount(lv.aggregates).max()) for lv in h.levels
+           if lv.aggregates is not None]
+    assert max(big) > 8, big
+    b = rng.standard_normal((9, g.n))
+    b -= b.mean(axis=1, keepdims=True)
+    x = np.stack([p.values for p in P.solve_many(h, b)])
+    dense = lap.toarray()
+    for r in range(3):
+        ref = dense_solve(dense, b[r])
+        assert np.abs(x[r] - ref).max() <= 1e-7 * np.abs(ref).max()
+    one = P.solve(h, b[4]).values
+    assert np.array_equal(one, x[4])
+
+
+def test_tolerance_not_baked_into_solve_graph(rng):
+    """The solve loop runs as a captured CUDA graph; its stop rule must follow
+    each call's tau (regression: a graph captured for one tau was replayed for
+    another)."""
+    g = G.grid_graph(32)
+    h = P.setup(P.laplacian(g))
+    b = rng.standard_normal(g.n)
+    b -= b.mean()
+    tight = P.solve(h, b, P.SolverConfig(tau=1e-12))
+    loose = P.solve(h, b, P.SolverConfig(tau=1e-3))
+    tight2 = P.solve(h, b, P.SolverConfig(tau=1e-12))
+    assert tight.achieved_residual <= 1e-12 and tight2.achieved_residual <= 1e-12
+    assert 1e-9 < loose.achieved_residual <= 1e-3
+    assert np.array_equal(tight.values, tight2.values)
