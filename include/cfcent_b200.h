@@ -204,6 +204,12 @@ int cf_build_csr(int64_t n, int64_t m, const int64_t* u, const int64_t* v, const
  * Gauss-Seidel, the B200 smoother ordering). */
 int cf_setup_colour(int64_t n, const int64_t* indptr, const int64_t* indices,
                     int32_t* out_colour, int32_t* n_colors);
+/* locality renumbering for the device copy: output row r = input row
+ * rows[r], columns mapped through cmap, rows sorted (scipy
+ * A[rows][:, order].sort_indices() with cmap = inverse(order)), threaded. */
+int cf_setup_permute(int64_t nrows, const int64_t* indptr, const int64_t* indices,
+                     const double* data, const int64_t* rows, const int64_t* cmap,
+                     int64_t* out_ptr, int64_t* out_idx, double* out_val);
 
 #ifdef __cplusplus
 }

@@ -95,6 +95,7 @@ _SIGS = {
                                      C.c_double, i64p, i64p]),
     "cf_setup_matching": (C.c_int, [C.c_int64, C.c_int64, i64p, i64p, i64p, i64p, i64p]),
     "cf_setup_colour": (C.c_int, [C.c_int64, i64p, i64p, i32p, i32p]),
+    "cf_setup_permute": (C.c_int, [C.c_int64, i64p, i64p, f64p, i64p, i64p, i64p, i64p, f64p]),
     "cf_rebuild_laplacian": (C.c_int, [C.c_int64, i64p, i64p, f64p, i64p, i64p, f64p, i64p]),
     "cf_build_csr": (C.c_int, [C.c_int64, C.c_int64, i64p, i64p, f64p, i64p, i64p, f64p, i64p]),
 }

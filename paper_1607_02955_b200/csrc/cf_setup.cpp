@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <thread>
 #include <vector>
 
 #include "cfcent_b200.h"
@@ -219,18 +220,47 @@ extern "C" int cf_rebuild_laplacian(int64_t n, const int64_t* indptr, const int6
     // indices.  Input: CSR without duplicate entries (any column order).
     CF_API_BEGIN
     const int64_t nnz = indptr[n];
-    // transpose by counting sort
+    // transpose by counting sort, threaded over row ranges: thread t scatters
+    // its rows after the entries of threads < t in every column, so each
+    // column lists its rows in ascending order (as a sequential pass would)
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const int64_t nt = std::min<int64_t>(hw, std::max<int64_t>(1, n / 4096));
+    std::vector<int64_t> cut(nt + 1, n);
+    cut[0] = 0;
+    for (int64_t t = 1; t < nt; ++t)
+        cut[t] = std::upper_bound(indptr, indptr + n + 1, nnz * t / nt) - indptr - 1;
+    for (int64_t t = 1; t <= nt; ++t) cut[t] = std::max(cut[t], cut[t - 1]);
+    auto run = [&](auto&& fn) {
+        std::vector<std::thread> th;
+        for (int64_t t = 0; t < nt; ++t) th.emplace_back(fn, t);
+        for (auto& x : th) x.join();
+    };
+    std::vector<std::vector<int64_t>> tcnt(nt, std::vector<int64_t>(n, 0));
+    run([&](int64_t t) {
+        auto& c = tcnt[t];
+        for (int64_t p = indptr[cut[t]]; p < indptr[cut[t + 1]]; ++p) ++c[indices[p]];
+    });
     std::vector<int64_t> tptr(n + 1, 0);
-    for (int64_t p = 0; p < nnz; ++p) ++tptr[indices[p] + 1];
-    for (int64_t i = 0; i < n; ++i) tptr[i + 1] += tptr[i];
-    std::vector<int64_t> tpos(tptr.begin(), tptr.end() - 1), tidx(nnz);
-    std::vector<double> tval(nnz);
-    for (int64_t i = 0; i < n; ++i)
-        for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) {
-            int64_t q = tpos[indices[p]]++;
-            tidx[q] = i;
-            tval[q] = data[p];
+    for (int64_t c = 0; c < n; ++c) {
+        int64_t s = tptr[c];
+        for (int64_t t = 0; t < nt; ++t) {
+            const int64_t k = tcnt[t][c];
+            tcnt[t][c] = s;  // thread t's first slot in column c
+            s += k;
         }
+        tptr[c + 1] = s;
+    }
+    std::vector<int64_t> tidx(nnz);
+    std::vector<double> tval(nnz);
+    run([&](int64_t t) {
+        auto& pos = tcnt[t];
+        for (int64_t i = cut[t]; i < cut[t + 1]; ++i)
+            for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) {
+                const int64_t q = pos[indices[p]]++;
+                tidx[q] = i;
+                tval[q] = data[p];
+            }
+    });
     // scipy adds M + M^T with its canonical kernel (sorted output) when both
     // operands have sorted, duplicate-free rows, else with the general kernel
     // whose rows come out in reverse first-appearance order (M's row in
@@ -242,64 +272,131 @@ extern "C" int cf_rebuild_laplacian(int64_t n, const int64_t* indptr, const int6
                 canonical = false;
                 break;
             }
-    std::vector<double> acc(n, 0.0);
-    std::vector<int64_t> mark(n, -1), cols, appear;
+    // rows are independent given the transpose: threads take row ranges of
+    // equal entry counts, write into local buffers, then concatenate in order
+    std::vector<std::vector<int64_t>> lidx(nt), lcnt(nt);
+    std::vector<std::vector<double>> lval(nt);
+    auto work = [&](int64_t t) {
+        std::vector<double> acc(n, 0.0);
+        std::vector<int64_t> mark(n, -1), cols, appear;
+        auto& oi = lidx[t];
+        auto& ov = lval[t];
+        auto& oc = lcnt[t];
+        oc.reserve((size_t)(cut[t + 1] - cut[t]));
+        for (int64_t i = cut[t]; i < cut[t + 1]; ++i) {
+            const size_t start = oi.size();
+            appear.clear();
+            for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) {
+                int64_t j = indices[p];
+                if (mark[j] != i) {
+                    mark[j] = i;
+                    acc[j] = 0.0;
+                    appear.push_back(j);
+                }
+                acc[j] += data[p];
+            }
+            for (int64_t p = tptr[i]; p < tptr[i + 1]; ++p) {
+                int64_t j = tidx[p];
+                if (mark[j] != i) {
+                    mark[j] = i;
+                    acc[j] = 0.0;
+                    appear.push_back(j);
+                }
+                acc[j] += tval[p];
+            }
+            cols.assign(appear.begin(), appear.end());
+            std::sort(cols.begin(), cols.end());
+            double dg = 0.0;
+            if (canonical) {
+                for (int64_t j : cols) {
+                    double v = acc[j] * 0.5;
+                    if (j != i && v < 0.0) dg += -v;
+                }
+            } else {
+                for (auto it = appear.rbegin(); it != appear.rend(); ++it) {
+                    int64_t j = *it;
+                    double v = acc[j] * 0.5;
+                    if (j != i && v < 0.0) dg += -v;
+                }
+            }
+            bool placed = false;
+            for (int64_t j : cols) {
+                if (!placed && j > i) {
+                    oi.push_back(i);
+                    ov.push_back(dg);
+                    placed = true;
+                }
+                double v = acc[j] * 0.5;
+                if (j != i && v < 0.0) {
+                    oi.push_back(j);
+                    ov.push_back(v);
+                }
+            }
+            if (!placed) {
+                oi.push_back(i);
+                ov.push_back(dg);
+            }
+            oc.push_back((int64_t)(oi.size() - start));
+        }
+    };
+    {
+        std::vector<std::thread> th;
+        for (int64_t t = 0; t < nt; ++t) th.emplace_back(work, t);
+        for (auto& x : th) x.join();
+    }
+
     int64_t out = 0;
     out_ptr[0] = 0;
-    for (int64_t i = 0; i < n; ++i) {
-        appear.clear();
-        for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) {
-            int64_t j = indices[p];
-            if (mark[j] != i) {
-                mark[j] = i;
-                acc[j] = 0.0;
-                appear.push_back(j);
-            }
-            acc[j] += data[p];
+    for (int64_t t = 0; t < nt; ++t) {
+        std::memcpy(out_idx + out, lidx[t].data(), sizeof(int64_t) * lidx[t].size());
+        std::memcpy(out_val + out, lval[t].data(), sizeof(double) * lval[t].size());
+        for (size_t r = 0; r < lcnt[t].size(); ++r) {
+            const int64_t i = cut[t] + (int64_t)r;
+            out_ptr[i + 1] = out_ptr[i] + lcnt[t][r];
         }
-        for (int64_t p = tptr[i]; p < tptr[i + 1]; ++p) {
-            int64_t j = tidx[p];
-            if (mark[j] != i) {
-                mark[j] = i;
-                acc[j] = 0.0;
-                appear.push_back(j);
-            }
-            acc[j] += tval[p];
-        }
-        cols.assign(appear.begin(), appear.end());
-        std::sort(cols.begin(), cols.end());
-        double dg = 0.0;
-        if (canonical) {
-            for (int64_t j : cols) {
-                double v = acc[j] * 0.5;
-                if (j != i && v < 0.0) dg += -v;
-            }
-        } else {
-            for (auto it = appear.rbegin(); it != appear.rend(); ++it) {
-                int64_t j = *it;
-                double v = acc[j] * 0.5;
-                if (j != i && v < 0.0) dg += -v;
-            }
-        }
-        bool placed = false;
-        for (int64_t j : cols) {
-            if (!placed && j > i) {
-                out_idx[out] = i;
-                out_val[out++] = dg;
-                placed = true;
-            }
-            double v = acc[j] * 0.5;
-            if (j != i && v < 0.0) {
-                out_idx[out] = j;
-                out_val[out++] = v;
-            }
-        }
-        if (!placed) {
-            out_idx[out] = i;
-            out_val[out++] = dg;
-        }
-        out_ptr[i + 1] = out;
+        out += (int64_t)lidx[t].size();
     }
     *nnz_out = out;
     CF_API_END
+}
+
+// Permuted CSR for the device upload (solver.py permute_levels): output row r
+// is input row rows[r]; an entry (j, v) becomes (cmap[j], v); every output row
+// is sorted by column.  Equivalent to scipy's A[rows][:, order] + sort_indices
+// with cmap = inverse of order, threaded over rows.  out_ptr: nrows + 1.
+extern "C" int cf_setup_permute(int64_t nrows, const int64_t* indptr, const int64_t* indices,
+                                const double* data, const int64_t* rows, const int64_t* cmap,
+                                int64_t* out_ptr, int64_t* out_idx, double* out_val) {
+    out_ptr[0] = 0;
+    for (int64_t r = 0; r < nrows; ++r)
+        out_ptr[r + 1] = out_ptr[r] + (indptr[rows[r] + 1] - indptr[rows[r]]);
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const int64_t nt = std::min<int64_t>(hw, std::max<int64_t>(1, nrows / 4096));
+    auto work = [&](int64_t r0, int64_t r1) {
+        std::vector<std::pair<int64_t, double>> tmp;
+        for (int64_t r = r0; r < r1; ++r) {
+            const int64_t a = indptr[rows[r]], b = indptr[rows[r] + 1], o = out_ptr[r];
+            tmp.resize((size_t)(b - a));
+            for (int64_t p = a; p < b; ++p) tmp[(size_t)(p - a)] = {cmap[indices[p]], data[p]};
+            std::sort(tmp.begin(), tmp.end(),
+                      [](const std::pair<int64_t, double>& x, const std::pair<int64_t, double>& y) {
+                          return x.first < y.first;
+                      });
+            for (int64_t q = 0; q < b - a; ++q) {
+                out_idx[o + q] = tmp[(size_t)q].first;
+                out_val[o + q] = tmp[(size_t)q].second;
+            }
+        }
+    };
+    // row ranges of equal entry counts (hub rows would unbalance equal row counts)
+    std::vector<int64_t> cut(nt + 1, nrows);
+    cut[0] = 0;
+    for (int64_t t = 1; t < nt; ++t)
+        cut[t] = std::upper_bound(out_ptr, out_ptr + nrows + 1, out_ptr[nrows] * t / nt) - out_ptr - 1;
+    for (int64_t t = 1; t <= nt; ++t) cut[t] = std::max(cut[t], cut[t - 1]);
+    std::vector<std::thread> th;
+    for (int64_t t = 0; t < nt; ++t)
+        th.emplace_back(work, cut[t], cut[t + 1]);
+    for (auto& x : th) x.join();
+    return CF_OK;
 }

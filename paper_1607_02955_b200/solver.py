@@ -65,7 +65,7 @@ DEVICE_DIRECT_FRACTION = 1.0 / 16.0
 # Locality ordering of the device copy: every non-dense level is
 # renumbered by reverse Cuthill-McKee so neighbour gathers of the row-major
 # blocks hit L2; the permutation is applied at the API boundary.
-DEVICE_REORDER = True
+DEVICE_REORDER = os.environ.get("CF_DEVICE_REORDER", "1") != "0"
 # Stall breaker (B200 setup): on power-law graphs the reference's
 # stages shrink a level by ~0.01-1 % for thousands of levels (R-MAT scale 20:
 # 2,859 levels).  When both reference stages miss MIN_REDUCTION, the setup
@@ -198,6 +198,32 @@ def _identity(n):
     return np.arange(n, dtype=np.int64)
 
 
+def _inverse(p):
+    inv = np.empty_like(p)
+    inv[p] = np.arange(p.size, dtype=p.dtype)
+    return inv
+
+
+def _permute(A: sp.csr_matrix, rows: np.ndarray, cmap: np.ndarray, ncols: int) -> sp.csr_matrix:
+    """A[rows][:, inverse(cmap)] with sorted rows (native, threaded)."""
+    A = A.tocsr()
+    ip, ix = _csr64(A)
+    val = np.ascontiguousarray(A.data, dtype=np.float64)
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    cmap = np.ascontiguousarray(cmap, dtype=np.int64)
+    nnz = int(np.sum(ip[rows + 1] - ip[rows])) if rows.size else 0
+    op = np.empty(rows.size + 1, dtype=np.int64)
+    oi = np.empty(nnz, dtype=np.int64)
+    ov = np.empty(nnz, dtype=np.float64)
+    N.check(N.lib().cf_setup_permute(rows.size, N.ptr(ip, N.i64p), N.ptr(ix, N.i64p),
+                                     N.ptr(val, N.f64p), N.ptr(rows, N.i64p),
+                                     N.ptr(cmap, N.i64p), N.ptr(op, N.i64p), N.ptr(oi, N.i64p),
+                                     N.ptr(ov, N.f64p)))
+    out = sp.csr_matrix((ov, oi, op), shape=(rows.size, ncols))
+    out.has_sorted_indices = True
+    return out
+
+
 def permute_levels(levels: list[Level]):
     """Renumber each non-dense level by RCM; returns (levels', perm0) with
     perm0[i'] = original node of device row i' on level 0.  Transfer
@@ -215,7 +241,7 @@ def permute_levels(levels: list[Level]):
         if lvl.kind is LevelKind.AGGREGATION:
             # colour classes of the RCM-ordered matrix become contiguous row
             # ranges (RCM order kept inside each class)
-            col = _colour(A[p][:, p].tocsr())
+            col = _colour(_permute(A, p, _inverse(p), p.size))
             order = np.argsort(col, kind="stable")
             p = p[order]
             classes[-1] = col[order]
@@ -231,8 +257,7 @@ def permute_levels(levels: list[Level]):
         if lvl.kind is LevelKind.COARSEST:
             out.append(lvl)
             continue
-        A = lvl.matrix.tocsr()[p][:, p].tocsr()
-        A.sort_indices()
+        A = _permute(lvl.matrix, p, inv, p.size)
         pn, invn = perms[j + 1], invs[j + 1]
         if lvl.kind is LevelKind.AGGREGATION:
             agg = invn[lvl.aggregates[p]]
@@ -241,8 +266,9 @@ def permute_levels(levels: list[Level]):
         else:
             f_new = inv[lvl.f_nodes]
             order = np.argsort(f_new, kind="stable")
-            w_cf = lvl.w_cf.tocsr()[pn][:, order].tocsr()
-            w_cf.sort_indices()
+            rank = np.empty_like(order)
+            rank[order] = np.arange(order.size)
+            w_cf = _permute(lvl.w_cf, pn, rank, order.size)
             out.append(Level(kind=LevelKind.ELIMINATION, matrix=A, f_nodes=f_new[order],
                              c_nodes=inv[lvl.c_nodes[pn]], f_degree=lvl.f_degree[order],
                              w_cf=w_cf, w_fc=w_cf.T.tocsr()))
