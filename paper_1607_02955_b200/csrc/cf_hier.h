@@ -135,6 +135,15 @@ struct Hier {
     int prof_begin(const char* kind, int level, double bytes, double gbytes);
     void prof_end(int idx);
 
+    // multi-block pinned transfers overlapped with the solve (cf_solve_rows):
+    // copy stream, double-buffered rows-layout staging in/out, n0 x pipe_kc
+    cudaStream_t cs = nullptr;
+    double* pin[2] = {nullptr, nullptr};
+    double* pout[2] = {nullptr, nullptr};
+    int pipe_kc = 0;
+    cudaEvent_t ev_in[2] = {}, ev_in_free[2] = {}, ev_out_ready[2] = {}, ev_out_done[2] = {};
+    void ensure_pipe(int kc);
+
     void* stage_host = nullptr;       // pinned staging ring for pageable transfers
     cudaEvent_t stage_ev[4] = {nullptr, nullptr, nullptr, nullptr};
     void ensure_stage();

@@ -1625,6 +1625,14 @@ Hier::~Hier() {
     cudaFree(SP);
     cudaFree(T);
     cudaFree(S);
+    cudaFree(PP);
+    for (int i = 0; i < 2; ++i) {
+        cudaFree(pin[i]);
+        cudaFree(pout[i]);
+        for (cudaEvent_t e : {ev_in[i], ev_in_free[i], ev_out_ready[i], ev_out_done[i]})
+            if (e) cudaEventDestroy(e);
+    }
+    if (cs) cudaStreamDestroy(cs);
     if (h_count) cudaFreeHost(h_count);
     if (stage_host) cudaFreeHost(stage_host);
     for (auto& e : stage_ev)
@@ -1746,6 +1754,28 @@ static void par_memcpy(void* dst, const void* src, size_t bytes) {
         th.emplace_back([=] { std::memcpy((char*)dst + a, (const char*)src + a, b - a); });
     }
     for (auto& x : th) x.join();
+}
+
+void Hier::ensure_pipe(int kc) {
+    if (!cs) {
+        CF_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i)
+            for (cudaEvent_t* e : {&ev_in[i], &ev_in_free[i], &ev_out_ready[i], &ev_out_done[i]}) {
+                CF_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+                CF_CUDA(cudaEventRecord(*e, s));  // "free" until first use
+            }
+    }
+    if (kc <= pipe_kc) return;
+    CF_CUDA(cudaStreamSynchronize(s));
+    CF_CUDA(cudaStreamSynchronize(cs));
+    for (int i = 0; i < 2; ++i) {
+        cudaFree(pin[i]);
+        cudaFree(pout[i]);
+        pin[i] = pout[i] = nullptr;
+        CF_CUDA(cudaMalloc(&pin[i], sizeof(double) * (size_t)n0 * kc));
+        CF_CUDA(cudaMalloc(&pout[i], sizeof(double) * (size_t)n0 * kc));
+    }
+    pipe_kc = kc;
 }
 
 void Hier::ensure_stage() {
@@ -2073,6 +2103,53 @@ extern "C" int cf_solve_rows(void* hp, const double* rows, int64_t count,
     CF_CUDA(cudaSetDevice(h.dev));
     const int64_t n = h.n0;
     int64_t done = 0;
+    if (count > pick_kc(count) && host_pinned(rows) && host_pinned(out_rows)) {
+        // several blocks, page-locked host buffers: block b+1's supplies are
+        // copied in and block b-1's solutions copied out on the copy stream
+        // while block b solves (double-buffered rows-layout staging)
+        std::vector<int64_t> off, num;
+        std::vector<int> kcs;
+        for (int64_t o = 0; o < count;) {
+            const int kc = pick_kc(count - o);
+            const int64_t c = std::min<int64_t>(kc, count - o);
+            off.push_back(o);
+            num.push_back(c);
+            kcs.push_back(kc);
+            o += c;
+        }
+        const int kmax = *std::max_element(kcs.begin(), kcs.end());
+        h.ensure_workspace(kmax);
+        h.ensure_pipe(kmax);
+        const size_t nb = off.size();
+        auto issue_in = [&](size_t b) {
+            const int q = (int)(b & 1);
+            CF_CUDA(cudaStreamWaitEvent(h.cs, h.ev_in_free[q], 0));
+            CF_CUDA(cudaMemcpyAsync(h.pin[q], rows + off[b] * n, sizeof(double) * num[b] * n,
+                                    cudaMemcpyHostToDevice, h.cs));
+            CF_CUDA(cudaEventRecord(h.ev_in[q], h.cs));
+        };
+        issue_in(0);
+        for (size_t b = 0; b < nb; ++b) {
+            const int q = (int)(b & 1);
+            if (b + 1 < nb) issue_in(b + 1);
+            CF_CUDA(cudaStreamWaitEvent(h.s, h.ev_in[q], 0));
+            rows_to_block(h, h.pin[q], (int)num[b], kcs[b], h.B);
+            CF_CUDA(cudaEventRecord(h.ev_in_free[q], h.s));
+            std::vector<double> res(kcs[b], 0.0);
+            solve_block(h, kcs[b], (int)num[b], *p, res.data(), *st);
+            CF_CUDA(cudaStreamWaitEvent(h.s, h.ev_out_done[q], 0));
+            block_to_rows(h, h.X, (int)num[b], kcs[b], h.pout[q]);
+            CF_CUDA(cudaEventRecord(h.ev_out_ready[q], h.s));
+            CF_CUDA(cudaStreamWaitEvent(h.cs, h.ev_out_ready[q], 0));
+            CF_CUDA(cudaMemcpyAsync(out_rows + off[b] * n, h.pout[q], sizeof(double) * num[b] * n,
+                                    cudaMemcpyDeviceToHost, h.cs));
+            CF_CUDA(cudaEventRecord(h.ev_out_done[q], h.cs));
+            std::memcpy(residuals + off[b], res.data(), sizeof(double) * num[b]);
+        }
+        CF_CUDA(cudaStreamSynchronize(h.s));
+        CF_CUDA(cudaStreamSynchronize(h.cs));
+        done = count;
+    }
     while (done < count) {
         int kc = pick_kc(count - done);
         int cnt = (int)std::min<int64_t>(kc, count - done);

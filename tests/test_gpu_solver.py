@@ -243,3 +243,23 @@ def test_tolerance_not_baked_into_solve_graph(rng):
     assert tight.achieved_residual <= 1e-12 and tight2.achieved_residual <= 1e-12
     assert 1e-9 < loose.achieved_residual <= 1e-3
     assert np.array_equal(tight.values, tight2.values)
+
+
+def test_pinned_multiblock_overlap_matches(rng):
+    """More right-hand sides than one device block with page-locked host
+    buffers take the overlapped copy-in / solve / copy-out pipeline; results
+    are bitwise those of the pageable path and of single solves."""
+    import torch
+    g = G.barabasi_albert_graph(5000, 3, 3)
+    h = P.setup(P.laplacian(g), P.SolverConfig(tau=1e-8))
+    k = 300  # 128 + 128 + 44 columns
+    b = rng.standard_normal((k, g.n))
+    b -= b.mean(axis=1, keepdims=True)
+    ref = np.stack([p.values for p in P.solve_many(h, b)])
+    b_pin = torch.empty(b.shape, dtype=torch.float64, pin_memory=True).numpy()
+    b_pin[:] = b
+    out = torch.empty(b.shape, dtype=torch.float64, pin_memory=True).numpy()
+    pots = P.solve_many(h, b_pin, out=out)
+    assert np.array_equal(out, ref)
+    assert all(p.achieved_residual <= 1e-8 for p in pots)
+    assert np.array_equal(P.solve(h, b[257]).values, ref[257])
