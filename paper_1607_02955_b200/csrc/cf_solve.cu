@@ -68,28 +68,23 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : CF_RED_CTAS)) k_res
     zero(loc[0]);
     zero(loc[1]);
     const int64_t part = blockIdx.x;
-    if (lane_ok) {
-        const int64_t r0 = part * kRowsPerPart;
-        row_pipeline<KC, G_PLAIN>(
-            r0 + slot, Lt::RPB, min((int64_t)n, r0 + kRowsPerPart), [](int64_t t) { return t; },
-            rp, col, val, nullptr, nullptr,
-            [&](int64_t, int64_t i, int64_t beg, int64_t end, int jj, double aa, double dd) {
-                DV<V> acc;
-                zero(acc);
-                row_sum_from<KC, G_PLAIN>(H, i, col, val, beg, end, nullptr, nullptr, X, c0, acc,
-                                          jj, aa, dd);
-                DV<V> b = ldv<V>(B + i * KC + c0), x = ldv<V>(X + i * KC + c0);
-                const double d = diag[i];
-                DV<V> out;
+    for (int r = slot; r < kRowsPerPart; r += Lt::RPB) {
+        int64_t i = part * kRowsPerPart + r;
+        if (i >= n || !lane_ok) break;
+        DV<V> acc;
+        zero(acc);
+        row_sum<KC, G_PLAIN>(H, i, col, val, rp[i], rp[i + 1], nullptr, nullptr, X, c0, acc);
+        DV<V> b = ldv<V>(B + i * KC + c0), x = ldv<V>(X + i * KC + c0);
+        double d = diag[i];
+        DV<V> out;
 #pragma unroll
-                for (int t = 0; t < V; ++t) {
-                    double v = b.v[t] - fma(d, x.v[t], acc.v[t]);
-                    out.v[t] = v;
-                    loc[0].v[t] += v;
-                    loc[1].v[t] = fma(v, v, loc[1].v[t]);
-                }
-                if (R) stv<V>(R + i * KC + c0, out);
-            });
+        for (int t = 0; t < V; ++t) {
+            double v = b.v[t] - fma(d, x.v[t], acc.v[t]);
+            out.v[t] = v;
+            loc[0].v[t] += v;
+            loc[1].v[t] = fma(v, v, loc[1].v[t]);
+        }
+        if (R) stv<V>(R + i * KC + c0, out);
     }
     cta_reduce_finish<KC, 2>(loc, smem, red, part);
 }
