@@ -125,7 +125,7 @@ struct Hier {
     std::map<int, cudaGraphExec_t> cycle_graphs;  // per KC
     std::map<int, cudaGraphExec_t> loop_graphs;   // whole outer iteration (while node)
     int *d_iter = nullptr, *d_ncyc = nullptr;
-    double* d_lp = nullptr;  // solve-loop parameters read by the status kernel
+    double* d_lp = nullptr;  // solve-loop parameters read by the status kernel (6)
     long long* d_vcyc = nullptr;
     bool prof = false;
     bool host_loop = false;  // CF_HOST_LOOP=1

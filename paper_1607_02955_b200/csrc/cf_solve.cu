@@ -34,7 +34,8 @@ namespace cf {
 static thread_local std::string g_last_error;
 void set_error(const std::string& m) { g_last_error = m; }
 
-enum ColState { COL_ZERO = 0, COL_ACTIVE = 1, COL_CONV = 2, COL_FALLBACK = 3 };
+// COL_KRYLOV: slowly converging column handed to V-cycle-preconditioned FCG
+enum ColState { COL_ZERO = 0, COL_ACTIVE = 1, COL_CONV = 2, COL_FALLBACK = 3, COL_KRYLOV = 4 };
 
 // ============================================================================
 // kernels
@@ -212,8 +213,8 @@ __global__ void k_status_loop(int n, const double* __restrict__ sums,
     CF_PDL_ENTRY();
     // loop parameters live in device memory so a captured solve graph serves
     // every tolerance (they are not baked into the graph)
-    const double stop = ctl.lp[0], sfac = ctl.lp[1];
-    const int scyc = (int)ctl.lp[2], max_cycles = (int)ctl.lp[3];
+    const double stop = ctl.lp[0], sfac = ctl.lp[1], kfac = ctl.lp[5];
+    const int scyc = (int)ctl.lp[2], max_cycles = (int)ctl.lp[3], kcheck = (int)ctl.lp[4];
     const int c = threadIdx.x;
     const int check = *ctl.iter;
     const bool final_check = check >= max_cycles;
@@ -229,6 +230,8 @@ __global__ void k_status_loop(int n, const double* __restrict__ sums,
                 prev[c] = r;
                 if (conv)
                     state[c] = COL_CONV;
+                else if (check == kcheck && f > kfac)
+                    state[c] = COL_KRYLOV;
                 else if (stall[c] >= scyc)
                     state[c] = COL_FALLBACK;
             } else {
@@ -1183,8 +1186,10 @@ struct Ops {
             if (mask[c]) res[c] = std::sqrt(s[KC + c]) / bn[c];
     }
 
-    static void fcg(Hier& h, const std::vector<double>& bn, double tau, int nu1, int nu2,
-                    int iters, const std::vector<char>& mask0, std::vector<double>& res) {
+    // returns the column V-cycles executed
+    static int64_t fcg(Hier& h, const std::vector<double>& bn, double tau, int nu1, int nu2,
+                       int iters, const std::vector<char>& mask0, std::vector<double>& res) {
+        int64_t colcyc = 0;
         h.ensure_fallback(KC);
         std::vector<char> active = mask0, have(KC, 0);
         column_res(h, h.X, bn, active, res);
@@ -1198,6 +1203,7 @@ struct Ops {
                 any = any || active[c];
             }
             if (!any) break;
+            for (int c = 0; c < KC; ++c) colcyc += active[c] ? 1 : 0;
             // r = center(b - L x)
             residual(h, h.B, h.X, h.R, h.sums);
             host_sums(h, 2, s.data());
@@ -1254,6 +1260,7 @@ struct Ops {
             center_cols(h, h.X, active);
             column_res(h, h.X, bn, active, res);
         }
+        return colcyc;
     }
 
     static void jpcg(Hier& h, const std::vector<double>& bn, double tau, int iters,
@@ -1424,8 +1431,21 @@ static void solve_block_t(Hier& h, int ncols, const CfSolveParams& p, double* re
     int64_t fallback_cols = 0;
     if (nactive > 0) {
         // check 0 on the host path, then the device-controlled loop
-        const double lp[4] = {stop, p.stagnation_factor, (double)p.stagnation_cycles,
-                              (double)p.max_cycles};
+        // Krylov hand-off: a column whose residual shrank by less
+        // than kKrylovFactor in the cycle before check kKrylovCheck continues
+        // under FCG preconditioned by the same V-cycle (warm start)
+        static const int kKrylovCheck = [] {
+            const char* e = std::getenv("CF_KRYLOV_CHECK");
+            return e ? std::atoi(e) : 3;
+        }();
+        static const double kKrylovFactor = [] {
+            const char* e = std::getenv("CF_KRYLOV_FACTOR");
+            return e ? std::atof(e) : 0.3;
+        }();
+        const double lp[6] = {stop, p.stagnation_factor, (double)p.stagnation_cycles,
+                              (double)p.max_cycles,
+                              kKrylovCheck > 0 && kKrylovCheck < p.max_cycles ? (double)kKrylovCheck : -1.0,
+                              kKrylovFactor};
         CF_CUDA(cudaMemcpyAsync(h.d_lp, lp, sizeof lp, cudaMemcpyHostToDevice, h.s));
         CF_CUDA(cudaMemsetAsync(h.d_iter, 0, sizeof(int), h.s));
         CF_CUDA(cudaMemsetAsync(h.d_vcyc, 0, sizeof(long long), h.s));
@@ -1459,6 +1479,25 @@ static void solve_block_t(Hier& h, int ncols, const CfSolveParams& p, double* re
         CF_CUDA(cudaMemcpyAsync(res.data(), h.res, sizeof(double) * KC, cudaMemcpyDeviceToHost,
                                 h.s));
         CF_CUDA(cudaStreamSynchronize(h.s));
+        {
+            std::vector<char> kr(KC, 0);
+            bool any = false;
+            for (int c = 0; c < KC; ++c)
+                if (state[c] == COL_KRYLOV) {
+                    kr[c] = 1;
+                    any = true;
+                }
+            if (any) {
+                std::vector<double> rk(KC, 0.0);
+                st.vcycles += O::fcg(h, safe, stop, p.nu1, p.nu2,
+                                     std::max(1, p.max_cycles - kKrylovCheck), kr, rk);
+                for (int c = 0; c < KC; ++c)
+                    if (kr[c]) {
+                        state[c] = rk[c] <= stop ? COL_CONV : COL_FALLBACK;
+                        res[c] = rk[c];
+                    }
+            }
+        }
         std::vector<char> fb(KC, 0);
         for (int c = 0; c < KC; ++c)
             if (state[c] == COL_FALLBACK) {
@@ -2062,7 +2101,7 @@ extern "C" int cf_hier_create(int32_t nlev, const CfLevelDesc* ds, int32_t devic
         // cannot attribute kernels inside graphs with conditional nodes)
         if (const char* e = std::getenv("CF_HOST_LOOP")) h->host_loop = std::atoi(e) != 0;
         h->d_iter = (int*)h->dalloc(sizeof(int) * 4);
-        h->d_lp = (double*)h->dalloc(sizeof(double) * 4);
+        h->d_lp = (double*)h->dalloc(sizeof(double) * 8);
         h->d_ncyc = (int*)h->dalloc(sizeof(int) * 4);
         h->d_vcyc = (long long*)h->dalloc(sizeof(long long) * 2);
         CF_CUDA(cudaMallocHost(&h->h_count, sizeof(int) * 4));
