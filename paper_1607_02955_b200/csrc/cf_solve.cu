@@ -292,6 +292,111 @@ __global__ void __launch_bounds__(kThreads) k_update(int n, double* __restrict__
     stv<V>(X + i * KC + c0, x);
 }
 
+// ---- Krylov hand-off: FCG preconditioned by one V-cycle (solver.py:571-611
+// restated for the device; columns in state COL_KRYLOV).  Per iteration:
+// centre r; z = V-cycle(r); zc = z - mean(z); beta = (zc.Ld)/(d.Ld) against
+// the previous direction d; d = zc - beta d; Ld = L d; alpha = (r.d)/(d.Ld);
+// x += alpha d; r = b - L x; status.
+// (q0, q1) = (zc . AP, P . AP) with zc = C - csum / n
+template <int KC>
+__global__ void __launch_bounds__(kThreads) k_kry_beta(int n, const double* __restrict__ C,
+                                                       const double* __restrict__ csum,
+                                                       const double* __restrict__ P,
+                                                       const double* __restrict__ AP,
+                                                       RedCtl red) {
+    CF_PDL_ENTRY();
+    CF_LANE_SETUP(KC)
+    extern __shared__ double smem[];
+    DV<V> loc[2];
+    zero(loc[0]);
+    zero(loc[1]);
+    const int64_t part = blockIdx.x;
+    for (int r = slot; r < kRowsPerPart; r += Lt::RPB) {
+        int64_t i = part * kRowsPerPart + r;
+        if (i >= n || !lane_ok) break;
+        DV<V> z = ldv<V>(C + i * KC + c0), p = ldv<V>(P + i * KC + c0);
+        DV<V> ap = ldv<V>(AP + i * KC + c0);
+#pragma unroll
+        for (int t = 0; t < V; ++t) {
+            const double zc = z.v[t] - csum[c0 + t] / (double)n;
+            loc[0].v[t] = fma(zc, ap.v[t], loc[0].v[t]);
+            loc[1].v[t] = fma(p.v[t], ap.v[t], loc[1].v[t]);
+        }
+    }
+    cta_reduce_finish<KC, 2>(loc, smem, red, part);
+}
+// P = zc - beta P  (beta = q0/q1 if q1 > 0, else 0)
+template <int KC>
+__global__ void __launch_bounds__(kThreads) k_kry_dir(int n, const double* __restrict__ C,
+                                                      const double* __restrict__ csum,
+                                                      const double* __restrict__ q,
+                                                      double* __restrict__ P) {
+    CF_PDL_ENTRY();
+    CF_LANE_SETUP(KC)
+    int64_t i = (int64_t)blockIdx.x * Lt::RPB + slot;
+    if (i >= n || !lane_ok) return;
+    DV<V> z = ldv<V>(C + i * KC + c0), p = ldv_c<V>(P + i * KC + c0);
+#pragma unroll
+    for (int t = 0; t < V; ++t) {
+        const int c = c0 + t;
+        const double beta = q[KC + c] > 0.0 ? q[c] / q[KC + c] : 0.0;
+        p.v[t] = (z.v[t] - csum[c] / (double)n) - beta * p.v[t];
+    }
+    stv<V>(P + i * KC + c0, p);
+}
+// X += alpha P for Krylov columns (alpha = (r.P)/(P.AP) if P.AP > 0); d = (P.AP, R.P)
+template <int KC>
+__global__ void __launch_bounds__(kThreads) k_kry_step(int n, double* __restrict__ X,
+                                                       const double* __restrict__ P,
+                                                       const double* __restrict__ d,
+                                                       const int* __restrict__ state) {
+    CF_PDL_ENTRY();
+    CF_LANE_SETUP(KC)
+    int64_t i = (int64_t)blockIdx.x * Lt::RPB + slot;
+    if (i >= n || !lane_ok) return;
+    DV<V> x = ldv_c<V>(X + i * KC + c0), p = ldv<V>(P + i * KC + c0);
+#pragma unroll
+    for (int t = 0; t < V; ++t) {
+        const int c = c0 + t;
+        if (state[c] == COL_KRYLOV && d[c] > 0.0) x.v[t] = fma(d[KC + c] / d[c], p.v[t], x.v[t]);
+    }
+    stv<V>(X + i * KC + c0, x);
+}
+// status after an FCG iteration: residual norms of Krylov columns, stop at
+// lp[0] (0.9 tau) or after lp[6] iterations (-> fallback chain); means of R
+template <int KC>
+__global__ void k_kry_status(int n, const double* __restrict__ sums,
+                             const double* __restrict__ bn, double* __restrict__ res,
+                             int* __restrict__ state, double* __restrict__ mean,
+                             int* __restrict__ count, LoopCtl ctl, int* __restrict__ kiter,
+                             cudaGraphConditionalHandle cond, int use_cond) {
+    CF_PDL_ENTRY();
+    const double stop = ctl.lp[0];
+    const int kmax = (int)ctl.lp[6];
+    const int c = threadIdx.x;
+    const int it = *kiter + 1;
+    int a = 0;
+    if (c < KC) {
+        if (state[c] == COL_KRYLOV) {
+            const double r = sqrt(sums[KC + c]) / bn[c];
+            res[c] = r;
+            if (r <= stop)
+                state[c] = COL_CONV;
+            else if (it >= kmax)
+                state[c] = COL_FALLBACK;
+        }
+        mean[c] = sums[c] / (double)n;
+        a = (state[c] == COL_KRYLOV) ? 1 : 0;
+    }
+    a = __syncthreads_count(a);
+    if (c == 0) {
+        *count = a;
+        *kiter = it;
+        if (a > 0) *ctl.vcyc += a;
+        if (use_cond) cudaGraphSetConditional(cond, a > 0 ? 1u : 0u);
+    }
+}
+
 // Y = a*Y + b*U + d*W with per-column coefficients coef[0|1|2][KC]
 template <int KC>
 __global__ void __launch_bounds__(kThreads) k_lincomb(int n, double* __restrict__ Y,
@@ -1186,6 +1291,104 @@ struct Ops {
             if (mask[c]) res[c] = std::sqrt(s[KC + c]) / bn[c];
     }
 
+    // one FCG iteration of the Krylov hand-off (kernels above); R holds
+    // b - L x with its sums, mean = column means of R, P / AP the direction
+    static void krylov_iteration(Hier& h, int nu1, int nu2, cudaGraphConditionalHandle hc,
+                                 int use_cond) {
+        const int n = h.n0;
+        const int64_t np = nparts_of(n);
+        double* mean = h.sums + 2 * KC;
+        double* csum = h.sums + 3 * KC;
+        double* q = h.sums + 4 * KC;  // 2 x KC
+        double* dd = h.sums + 6 * KC; // 2 x KC
+        center(h, h.R, mean);
+        cycle(h, 0, nu1, nu2);
+        colsum(h, h.C, nullptr, csum);
+        {
+            ProfScope ps(h, "krylov", 0, 3.0 * Vb(n));
+            launch_k(k_kry_beta<KC>, dim3((unsigned)np), dim3(kThreads), red_smem<KC, 2>(), h.s,
+                     n, h.C, csum, h.P, h.AP, redctl(h, h.parts, np, q, 0));
+        }
+        {
+            ProfScope ps(h, "krylov", 0, 3.0 * Vb(n));
+            launch_k(k_kry_dir<KC>, dim3(grid_rows<KC>(n)), dim3(kThreads), 0, h.s, n, h.C, csum,
+                     q, h.P);
+        }
+        spmm(h, h.P, h.AP);
+        dot2(h, h.P, h.AP, h.R, h.P, dd);
+        {
+            ProfScope ps(h, "krylov", 0, 3.0 * Vb(n));
+            launch_k(k_kry_step<KC>, dim3(grid_rows<KC>(n)), dim3(kThreads), 0, h.s, n, h.X, h.P,
+                     dd, h.state);
+        }
+        residual(h, h.B, h.X, h.R, h.sums);
+        ProfScope ps(h, "status", 0, 0.0);
+        LoopCtl ctl{h.d_lp, h.d_iter, h.d_vcyc, h.d_ncyc};
+        launch_k(k_kry_status<KC>, dim3(1), dim3(KC < 32 ? 32 : KC), 0, h.s, n, h.sums, h.bn,
+                 h.res, h.state, mean, h.count, ctl, h.d_iter + 2, hc, use_cond);
+    }
+    static cudaGraphExec_t krylov_graph(Hier& h, int nu1, int nu2) {
+        const int key = -(KC * 1000000 + nu1 * 1000 + nu2);
+        auto it = h.loop_graphs.find(key);
+        if (it != h.loop_graphs.end()) return it->second;
+        cudaGraph_t g;
+        CF_CUDA(cudaGraphCreate(&g, 0));
+        cudaGraphConditionalHandle hc;
+        CF_CUDA(cudaGraphConditionalHandleCreate(&hc, g, 1, cudaGraphCondAssignDefault));
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = hc;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t node;
+        CF_CUDA(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        CF_CUDA(cudaStreamBeginCaptureToGraph(h.s, body, nullptr, nullptr, 0,
+                                              cudaStreamCaptureModeThreadLocal));
+        try {
+            krylov_iteration(h, nu1, nu2, hc, 1);
+        } catch (...) {
+            cudaGraph_t tmp;
+            cudaStreamEndCapture(h.s, &tmp);
+            cudaGraphDestroy(g);
+            throw;
+        }
+        cudaGraph_t captured;
+        CF_CUDA(cudaStreamEndCapture(h.s, &captured));
+        cudaGraphExec_t ge;
+        CF_CUDA(cudaGraphInstantiate(&ge, g, 0));
+        CF_CUDA(cudaGraphDestroy(g));
+        h.loop_graphs.emplace(key, ge);
+        return ge;
+    }
+    // Krylov hand-off driver: columns in COL_KRYLOV (R / sums / mean current
+    // for X) iterate until converged or kmax iterations; returns column cycles
+    static int64_t krylov(Hier& h, int nu1, int nu2, int kmax, int nkry) {
+        h.ensure_fallback(KC);
+        CF_CUDA(cudaMemsetAsync(h.P, 0, sizeof(double) * (size_t)h.n0 * KC, h.s));
+        CF_CUDA(cudaMemsetAsync(h.AP, 0, sizeof(double) * (size_t)h.n0 * KC, h.s));
+        const double kx = (double)kmax;
+        CF_CUDA(cudaMemcpyAsync(h.d_lp + 6, &kx, sizeof(double), cudaMemcpyHostToDevice, h.s));
+        CF_CUDA(cudaMemsetAsync(h.d_iter + 2, 0, sizeof(int), h.s));
+        CF_CUDA(cudaMemsetAsync(h.d_vcyc, 0, sizeof(long long), h.s));
+        long long vc0 = nkry;  // the first iteration's cycles (counted at its end only if still active)
+        if (h.prof || h.host_loop) {
+            *h.h_count = nkry;
+            for (int it = 0; it < kmax && *h.h_count > 0; ++it) {
+                krylov_iteration(h, nu1, nu2, cudaGraphConditionalHandle{}, 0);
+                CF_CUDA(cudaMemcpyAsync(h.h_count, h.count, sizeof(int), cudaMemcpyDeviceToHost,
+                                        h.s));
+                CF_CUDA(cudaStreamSynchronize(h.s));
+            }
+        } else {
+            CF_CUDA(cudaGraphLaunch(krylov_graph(h, nu1, nu2), h.s));
+        }
+        long long vc = 0;
+        CF_CUDA(cudaMemcpyAsync(&vc, h.d_vcyc, sizeof(long long), cudaMemcpyDeviceToHost, h.s));
+        CF_CUDA(cudaStreamSynchronize(h.s));
+        return vc0 + vc;
+    }
+
     // returns the column V-cycles executed
     static int64_t fcg(Hier& h, const std::vector<double>& bn, double tau, int nu1, int nu2,
                        int iters, const std::vector<char>& mask0, std::vector<double>& res) {
@@ -1488,14 +1691,15 @@ static void solve_block_t(Hier& h, int ncols, const CfSolveParams& p, double* re
                     any = true;
                 }
             if (any) {
-                std::vector<double> rk(KC, 0.0);
-                st.vcycles += O::fcg(h, safe, stop, p.nu1, p.nu2,
-                                     std::max(1, p.max_cycles - kKrylovCheck), kr, rk);
-                for (int c = 0; c < KC; ++c)
-                    if (kr[c]) {
-                        state[c] = rk[c] <= stop ? COL_CONV : COL_FALLBACK;
-                        res[c] = rk[c];
-                    }
+                int nk = 0;
+                for (int c = 0; c < KC; ++c) nk += kr[c];
+                st.vcycles += O::krylov(h, p.nu1, p.nu2, std::max(1, p.max_cycles - kKrylovCheck),
+                                        nk);
+                CF_CUDA(cudaMemcpyAsync(state.data(), h.state, sizeof(int) * KC,
+                                        cudaMemcpyDeviceToHost, h.s));
+                CF_CUDA(cudaMemcpyAsync(res.data(), h.res, sizeof(double) * KC,
+                                        cudaMemcpyDeviceToHost, h.s));
+                CF_CUDA(cudaStreamSynchronize(h.s));
             }
         }
         std::vector<char> fb(KC, 0);
