@@ -208,7 +208,10 @@ __device__ __forceinline__ void fetch_chunk(const int32_t* __restrict__ col,
 // coalesced access and broadcast them by shuffle; up to G neighbour rows are
 // then in flight per warp.  (jj, aa, dd) is the lane's share of the first chunk
 // (fetch_chunk at beg), which a row pipeline loads one row ahead.
-template <int KC, int MODE>
+#ifndef CF_GATHER_DOUBLES
+#define CF_GATHER_DOUBLES 16
+#endif
+template <int KC, int MODE, int GD = CF_GATHER_DOUBLES>
 __device__ __forceinline__ void gather_row_from(const int32_t* __restrict__ col,
                                                 const double* __restrict__ val, int64_t beg,
                                                 int64_t end, const int32_t* __restrict__ map,
@@ -220,12 +223,9 @@ __device__ __forceinline__ void gather_row_from(const int32_t* __restrict__ col,
     constexpr int V = Lay<KC>::VEC;
     constexpr int W = Lay<KC>::LPR;
     constexpr unsigned MASK = W == 32 ? 0xffffffffu : ((1u << W) - 1u);
-    // rows in flight per group: CF_GATHER_DOUBLES doubles of row data per lane,
-    // so the gather kernels fit 3 CTAs of 256 threads per SM
-#ifndef CF_GATHER_DOUBLES
-#define CF_GATHER_DOUBLES 16
-#endif
-    constexpr int G0 = CF_GATHER_DOUBLES / V;
+    // rows in flight per group: GD doubles of row data per lane (default
+    // CF_GATHER_DOUBLES, so the gather kernels fit 3 CTAs of 256 threads per SM)
+    constexpr int G0 = GD / V > 0 ? GD / V : 1;
     constexpr int G = W < G0 ? W : G0;
     int jn = 0;
     double an = 0.0, dn = 1.0;
@@ -265,7 +265,7 @@ __device__ __forceinline__ void gather_row_from(const int32_t* __restrict__ col,
     }
 }
 
-template <int KC, int MODE>
+template <int KC, int MODE, int GD = CF_GATHER_DOUBLES>
 __device__ __forceinline__ void gather_row(const int32_t* __restrict__ col,
                                            const double* __restrict__ val, int64_t beg,
                                            int64_t end, const int32_t* __restrict__ map,
@@ -275,7 +275,7 @@ __device__ __forceinline__ void gather_row(const int32_t* __restrict__ col,
     int jj;
     double aa, dd;
     fetch_chunk<KC, MODE>(col, val, map, div, beg, end, jj, aa, dd);
-    gather_row_from<KC, MODE>(col, val, beg, end, map, div, X, c0, acc, jj, aa, dd, jlim);
+    gather_row_from<KC, MODE, GD>(col, val, beg, end, map, div, X, c0, acc, jj, aa, dd, jlim);
 }
 
 // Row pipeline: a warp visits the rows row_of(t) for t = first, first + stride,

@@ -674,8 +674,10 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : CF_RED_CTAS)) k_eli
 }
 
 // Partial sums of heavy-row segments: P[s] = sum over [sbeg[s], send[s]).
-template <int KC, int MODE>
-__global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : kGatherCtas)) k_seg(int64_t s_lo, int64_t s_hi,
+// DEEP: launches with few segments (a handful per SM) are latency-bound, so
+// every warp keeps 4x the neighbour rows in flight (1 CTA/SM by registers).
+template <int KC, int MODE, bool DEEP = false>
+__global__ void __launch_bounds__(kThreads, DEEP ? 1 : (KC >= 256 ? 2 : kGatherCtas)) k_seg(int64_t s_lo, int64_t s_hi,
                                                   const int64_t* __restrict__ sbeg,
                                                   const int64_t* __restrict__ send,
                                                   const int32_t* __restrict__ col,
@@ -690,7 +692,8 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : kGatherCtas)) k_seg
     if (sg >= s_hi || !lane_ok) return;
     DV<V> acc;
     zero(acc);
-    gather_row<KC, MODE>(col, val, sbeg[sg], send[sg], map, div, X, c0, acc);
+    gather_row<KC, MODE, DEEP ? 4 * CF_GATHER_DOUBLES : CF_GATHER_DOUBLES>(
+        col, val, sbeg[sg], send[sg], map, div, X, c0, acc);
     stv<V>(P + (size_t)sg * KC + c0, acc);
 }
 
@@ -917,6 +920,10 @@ template <int KC>
 static inline unsigned grid_rows(int64_t rows, int64_t at_least = 1) {
     return (unsigned)std::max<int64_t>(at_least, (rows + Lay<KC>::RPB - 1) / Lay<KC>::RPB);
 }
+#ifndef CF_DEEP_SEG_CTAS
+#define CF_DEEP_SEG_CTAS 296
+#endif
+constexpr unsigned kDeepSegCtas = CF_DEEP_SEG_CTAS;  // <= 2 CTAs per SM: deep k_seg
 static inline unsigned grid_tiles(int64_t rows, int64_t at_least = 1, int rpw = kTileRows / kWarps) {
     const int64_t t = (int64_t)kWarps * rpw;
     return (unsigned)std::max<int64_t>(at_least, (rows + t - 1) / t);
@@ -988,7 +995,13 @@ struct Ops {
         const double hnnz = (lo == 0 && hi == pl.nseg) ? (double)pl.heavy_nnz
                                                        : (double)kSegNnz * (hi - lo);
         ProfScope ps(h, "heavy_seg", level, 12.0 * hnnz + Vb(hi - lo) * 2, Vb(hnnz));
-        launch_k(k_seg<KC, MODE>, dim3((unsigned)((hi - lo + Lay<KC>::RPB - 1) / Lay<KC>::RPB)), dim3(kThreads), 0, h.s, lo, hi, pl.sbeg, pl.send, col, val, map, div, X, h.SP);
+        const unsigned grid = (unsigned)((hi - lo + Lay<KC>::RPB - 1) / Lay<KC>::RPB);
+        if (grid <= kDeepSegCtas)
+            launch_k(k_seg<KC, MODE, true>, dim3(grid), dim3(kThreads), 0, h.s, lo, hi, pl.sbeg,
+                     pl.send, col, val, map, div, X, h.SP);
+        else
+            launch_k(k_seg<KC, MODE, false>, dim3(grid), dim3(kThreads), 0, h.s, lo, hi, pl.sbeg,
+                     pl.send, col, val, map, div, X, h.SP);
     }
     static void residual(Hier& h, const double* B, const double* X, double* R, double* sums2) {
         DLevel& l = h.L[0];
