@@ -178,6 +178,40 @@ enum GatherMode { G_PLAIN = 0, G_MAPPED = 1, G_ELIM = 2 };
 // The working lanes of the warp load LPR consecutive (col, val) pairs with one
 // coalesced access and broadcast them by shuffle; up to 8 neighbour rows are
 // then in flight per warp.
+// Streaming loads of matrix entries (read once per launch): with
+// CF_EVICT_FIRST they are marked L2::evict_first so they do not displace the
+// neighbour rows of X that later rows gather again.
+#ifndef CF_EVICT_FIRST
+#define CF_EVICT_FIRST 0
+#endif
+#if CF_EVICT_FIRST
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+#endif
+__device__ __forceinline__ int32_t ld_stream(const int32_t* p) {
+#if CF_EVICT_FIRST
+    int32_t v;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;"
+        : "=r"(v) : "l"(p), "l"(evict_first_policy()));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+__device__ __forceinline__ double ld_stream(const double* p) {
+#if CF_EVICT_FIRST
+    double v;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+        : "=d"(v) : "l"(p), "l"(evict_first_policy()));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+
 // A lane's share of one W-entry chunk of a CSR row: lane u < W holds entry
 // p0 + u (column, value and, for G_ELIM, the divisor), or zeros past `end`.
 template <int KC, int MODE>
@@ -192,8 +226,8 @@ __device__ __forceinline__ void fetch_chunk(const int32_t* __restrict__ col,
     aa = 0.0;
     dd = 1.0;
     if (p0 + lane < end && lane < W) {
-        jj = __ldg(col + p0 + lane);
-        aa = __ldg(val + p0 + lane);
+        jj = ld_stream(col + p0 + lane);
+        aa = ld_stream(val + p0 + lane);
         if constexpr (MODE == G_ELIM) dd = __ldg(div + jj);
         if constexpr (MODE != G_PLAIN) jj = __ldg(map + jj);
     }
