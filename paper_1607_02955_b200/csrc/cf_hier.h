@@ -46,6 +46,9 @@ struct DLevel {
     int32_t *pa = nullptr, *pb = nullptr, *pslot = nullptr;
     int* acnt = nullptr;  // split aggregate -> arrivals (zero between launches)
     int32_t *fn = nullptr, *cn = nullptr;
+    int32_t* cagg = nullptr;  // aggregation: agg[col[p]] per off-diagonal entry
+    int32_t* wcm = nullptr;   // elimination: fn[wcc[p]] per W_cf entry
+    double* wcd = nullptr;    // elimination: fd[wcc[p]] per W_cf entry
     double* fd = nullptr;
     int64_t* wcp = nullptr;
     int32_t* wcc = nullptr;

@@ -168,13 +168,15 @@ __device__ __forceinline__ void zero(DV<V>& r) {
 }
 
 // Gather modes: what the CSR entry (j, a) of a row multiplies.
-enum GatherMode { G_PLAIN = 0, G_MAPPED = 1, G_ELIM = 2 };
+enum GatherMode { G_PLAIN = 0, G_MAPPED = 1, G_ELIM = 2, G_DIV = 3 };
 
 // acc += sum_p val[p] * Y(col[p]) over p in [beg, end), ascending p (one fma
 // chain per column, identical for every block width), where
 //   G_PLAIN : Y(j) = X[j, :]
 //   G_MAPPED: Y(j) = X[map[j], :]                 (P xc gathers)
 //   G_ELIM  : Y(j) = X[map[j], :] / div[j]        (W_cf (b_f / d_f))
+//   G_DIV   : Y(j) = X[j, :] / div[p]             (G_ELIM with the map and the
+//             divisor resolved per entry at upload: one dependent load less)
 // The working lanes of the warp load LPR consecutive (col, val) pairs with one
 // coalesced access and broadcast them by shuffle; up to 8 neighbour rows are
 // then in flight per warp.
@@ -229,7 +231,8 @@ __device__ __forceinline__ void fetch_chunk(const int32_t* __restrict__ col,
         jj = ld_stream(col + p0 + lane);
         aa = ld_stream(val + p0 + lane);
         if constexpr (MODE == G_ELIM) dd = __ldg(div + jj);
-        if constexpr (MODE != G_PLAIN) jj = __ldg(map + jj);
+        if constexpr (MODE == G_DIV) dd = ld_stream(div + p0 + lane);
+        if constexpr (MODE == G_MAPPED || MODE == G_ELIM) jj = __ldg(map + jj);
     }
 }
 
@@ -238,6 +241,8 @@ __device__ __forceinline__ void fetch_chunk(const int32_t* __restrict__ col,
 //   G_PLAIN : Y(j) = X[j, :]
 //   G_MAPPED: Y(j) = X[map[j], :]                 (P xc gathers)
 //   G_ELIM  : Y(j) = X[map[j], :] / div[j]        (W_cf (b_f / d_f))
+//   G_DIV   : Y(j) = X[j, :] / div[p]             (G_ELIM with the map and the
+//             divisor resolved per entry at upload: one dependent load less)
 // The working lanes of the warp load LPR consecutive (col, val) pairs with one
 // coalesced access and broadcast them by shuffle; up to G neighbour rows are
 // then in flight per warp.  (jj, aa, dd) is the lane's share of the first chunk
@@ -274,7 +279,7 @@ __device__ __forceinline__ void gather_row_from(const int32_t* __restrict__ col,
             for (int u = 0; u < G; ++u) {
                 int j = __shfl_sync(MASK, jj, u0 + u, W);
                 a[u] = __shfl_sync(MASK, aa, u0 + u, W);
-                if constexpr (MODE == G_ELIM) d[u] = __shfl_sync(MASK, dd, u0 + u, W);
+                if constexpr (MODE == G_ELIM || MODE == G_DIV) d[u] = __shfl_sync(MASK, dd, u0 + u, W);
                 if (u0 + u < cnt && j < jlim)
                     x[u] = ldv<V>(X + (size_t)j * KC + c0);
                 else
@@ -285,7 +290,7 @@ __device__ __forceinline__ void gather_row_from(const int32_t* __restrict__ col,
                 if (u0 + u < cnt) {
 #pragma unroll
                     for (int t = 0; t < V; ++t) {
-                        if constexpr (MODE == G_ELIM)
+                        if constexpr (MODE == G_ELIM || MODE == G_DIV)
                             acc.v[t] = fma(a[u], x[u].v[t] / d[u], acc.v[t]);
                         else
                             acc.v[t] = fma(a[u], x[u].v[t], acc.v[t]);

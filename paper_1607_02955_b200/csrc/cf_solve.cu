@@ -609,7 +609,7 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : CF_RED_CTAS)) k_agg
             if (i >= n || !lane_ok) break;
             DV<V> acc;
             zero(acc);
-            row_sum<KC, G_MAPPED>(H, i, col, val, rp[i], rp[i + 1], agg, nullptr, Xc, c0, acc);
+            row_sum<KC, G_PLAIN>(H, i, col, val, rp[i], rp[i + 1], nullptr, nullptr, Xc, c0, acc);
             DV<V> d = ldv<V>(Xc + (size_t)agg[i] * KC + c0);
             double dg = diag[i];
 #pragma unroll
@@ -666,7 +666,7 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : CF_RED_CTAS)) k_eli
     if (i >= nc || !lane_ok) return;
     DV<V> acc;
     zero(acc);
-    row_sum<KC, G_ELIM>(H, i, wc, wv, wp[i], wp[i + 1], fn, fd, B, c0, acc);
+    row_sum<KC, G_DIV>(H, i, wc, wv, wp[i], wp[i + 1], nullptr, fd, B, c0, acc);
     DV<V> b = ldv<V>(B + (size_t)cn[i] * KC + c0);
 #pragma unroll
     for (int t = 0; t < V; ++t) acc.v[t] = b.v[t] + acc.v[t];
@@ -1079,12 +1079,12 @@ struct Ops {
         double* xc = bufx(h, j + 1);
         if (l.kind == CF_LEVEL_ELIMINATION) {
             {
-                seg<G_ELIM>(h, l.pw, 0, l.pw.nseg, l.wcc, l.wcv, l.fn, l.fd, b, j);
+                seg<G_DIV>(h, l.pw, 0, l.pw.nseg, l.wcm, l.wcv, nullptr, l.wcd, b, j);
                 ProfScope ps(h, "elim_restrict", j,
                              12.0 * (l.w_nnz - l.pw.heavy_nnz) + 12.0 * l.nc + 12.0 * l.nf +
                                  Vb(2 * l.nc + l.nf));
                 launch_k(k_elim_restrict<KC>, dim3(grid_rows<KC>(l.nc)), dim3(kThreads), 0, h.s,
-                         l.nc, l.cn, l.wcp, l.wcc, l.wcv, l.fn, l.fd, b, bc, hd(h, l.pw));
+                         l.nc, l.cn, l.wcp, l.wcm, l.wcv, nullptr, l.wcd, b, bc, hd(h, l.pw));
             }
             cycle(h, j + 1, nu1, nu2);
             ProfScope ps(h, "elim_interp", j,
@@ -1123,12 +1123,12 @@ struct Ops {
         cycle(h, j + 1, nu1, nu2);
         int64_t pf = nparts_of(l.n), pc = nparts_of(l.nc);
         {
-            seg<G_MAPPED>(h, l.pm, 0, l.pm.nseg, l.col, l.val, l.agg, nullptr, xc, j);
+            seg<G_PLAIN>(h, l.pm, 0, l.pm.nseg, l.cagg, l.val, nullptr, nullptr, xc, j);
             const int64_t light = l.nnz - l.pm.heavy_nnz;
             ProfScope ps(h, "agg_linesearch", j, A(l.n, light) + 4.0 * l.n + Vb(2 * l.nc),
                          Vb(light));
             launch_k(k_agg_ls<KC>, dim3((unsigned)(pf + pc)), dim3(kThreads), red_smem<KC, 1>(),
-                     h.s, l.n, l.nc, l.rp, l.col, l.val, l.diag, l.agg, xc, bc,
+                     h.s, l.n, l.nc, l.rp, l.cagg, l.val, l.diag, l.agg, xc, bc,
                      redctl(h, h.parts, pf, l.ls, 0), redctl(h, h.parts + pf * KC, pc, l.ls + KC, 1),
                      hd(h, l.pm));
         }
@@ -2210,6 +2210,14 @@ extern "C" int cf_hier_create(int32_t nlev, const CfLevelDesc* ds, int32_t devic
                 l.contig = true;
                 for (int32_t q = 0; q < d.n && l.contig; ++q) l.contig = d.color_rows[q] == q;
                 l.agg = upload(*h, d.agg, (size_t)d.n);
+                {
+                    // aggregate of every off-diagonal entry's column (line search
+                    // gathers X_c[agg[j]] without the dependent map load)
+                    std::vector<int32_t> ca((size_t)d.nnz_off);
+                    for (int64_t q = 0; q < d.nnz_off; ++q) ca[(size_t)q] = d.agg[d.col[q]];
+                    l.cagg = upload(*h, ca.data(), ca.size());
+                    if (!l.cagg) l.cagg = (int32_t*)h->dalloc(8);
+                }
                 l.aptr = upload(*h, d.agg_ptr, (size_t)d.n_coarse + 1);
                 l.amem = upload(*h, d.agg_members, (size_t)d.n);
                 {
@@ -2293,6 +2301,20 @@ extern "C" int cf_hier_create(int32_t nlev, const CfLevelDesc* ds, int32_t devic
                 l.wcp = upload(*h, d.wcf_ptr, (size_t)d.n_coarse + 1);
                 l.wcc = upload(*h, d.wcf_col, (size_t)d.wcf_ptr[d.n_coarse]);
                 l.wcv = upload(*h, d.wcf_val, (size_t)d.wcf_ptr[d.n_coarse]);
+                {
+                    // W_cf entries resolved to (fine node, its degree) at upload
+                    const int64_t wn = d.wcf_ptr[d.n_coarse];
+                    std::vector<int32_t> wm((size_t)wn);
+                    std::vector<double> wd((size_t)wn);
+                    for (int64_t q = 0; q < wn; ++q) {
+                        wm[(size_t)q] = d.f_nodes[d.wcf_col[q]];
+                        wd[(size_t)q] = d.f_degree[d.wcf_col[q]];
+                    }
+                    l.wcm = upload(*h, wm.data(), wm.size());
+                    l.wcd = upload(*h, wd.data(), wd.size());
+                    if (!l.wcm) l.wcm = (int32_t*)h->dalloc(8);
+                    if (!l.wcd) l.wcd = (double*)h->dalloc(8);
+                }
                 l.wfp = upload(*h, d.wfc_ptr, (size_t)d.n_f + 1);
                 l.w_nnz = d.wcf_ptr[d.n_coarse];
                 l.pw = build_plan(*h, d.n_coarse, d.wcf_ptr, nullptr, nullptr, 1);
