@@ -227,3 +227,42 @@ def test_native_csr_builder_matches_reference(rng):
         ip, ix, ww = O.graph_from_edges(u, v, w, n=n)
         assert np.array_equal(g.indptr, ip) and np.array_equal(g.indices, ix)
         assert np.array_equal(g.weights, ww)
+
+
+def test_native_permute_matches_scipy(rng):
+    """cf_setup_permute (device-upload renumbering) equals scipy's
+    A[rows][:, order] with sorted indices, square and rectangular."""
+    import scipy.sparse as sp
+    from paper_1607_02955_b200 import solver as S
+    for shape in ((300, 300), (120, 250)):
+        A = sp.random(*shape, density=0.05, random_state=np.random.RandomState(3), format="csr")
+        rows = rng.permutation(shape[0])
+        order = rng.permutation(shape[1])
+        cmap = np.empty_like(order)
+        cmap[order] = np.arange(order.size)
+        got = S._permute(A, rows, cmap, shape[1])
+        ref = A[rows][:, order].tocsr()
+        ref.sort_indices()
+        assert np.array_equal(got.indptr, ref.indptr)
+        assert np.array_equal(got.indices, ref.indices)
+        assert np.array_equal(got.data, ref.data)
+
+
+def test_hub_level_rule():
+    """Hub-level aggregation cap applies only to large graphs whose maximum
+    off-degree exceeds HUB_DEGREE_RATIO x the mean (R-MAT), never to grids."""
+    import scipy.sparse as sp
+    from paper_1607_02955_b200 import solver as S
+    n = 2000
+    # star + path: one hub of degree n-1
+    u = np.r_[np.zeros(n - 1, dtype=np.int64), np.arange(1, n - 1)]
+    v = np.r_[np.arange(1, n), np.arange(2, n)]
+    g = P.Graph.from_edges(u, v, np.ones(u.size), n=n)
+    lap = P.laplacian(g)
+    offdeg = np.diff(lap.indptr) - 1
+    assert offdeg.max() > S.HUB_DEGREE_RATIO * offdeg.mean()
+    assert S.HUB_AGG_CAP >= S.MAX_AGGREGATE_SIZE
+    # small graphs keep the reference cap: identical hierarchy with the rule off
+    h1 = P.setup(lap)
+    h2 = P.setup(lap, stall_breaker=False)
+    assert h1.level_sizes == h2.level_sizes
