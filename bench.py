@@ -51,8 +51,15 @@ def _peaks():
 
 
 class Clocks:
-    """nvidia-smi sampler running during the timed region."""
+    """SM clock / throttle-reason sampler running during the timed region:
+    NVML polled every 5 ms from a thread (so even a 50 ms region gets samples),
+    falling back to `nvidia-smi -lms 200` when NVML is unavailable.  The GPU is
+    addressed by the visible device's PCI bus id."""
 
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -61,8 +68,26 @@ class Clocks:
         self.index = index
         self.proc = None
         self.lines: list[str] = []
+        self.samples: list[tuple[float, int]] = []
+        self.smax = 0.0
+        self._stop = threading.Event()
+        self._nv = None
 
     def __enter__(self):
+        try:
+            import pynvml as nv
+            import torch
+            nv.nvmlInit()
+            pr = torch.cuda.get_device_properties(self.index)
+            bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+            self._h = nv.nvmlDeviceGetHandleByPciBusId(bus)
+            self.smax = float(nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM))
+            self._nv = nv
+            self._t = threading.Thread(target=self._poll, daemon=True)
+            self._t.start()
+            return self
+        except Exception:
+            self._nv = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
@@ -74,11 +99,24 @@ class Clocks:
             self.proc = None
         return self
 
+    def _poll(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append((float(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)),
+                                     int(nv.nvmlDeviceGetCurrentClocksEventReasons(self._h))))
+            except Exception:
+                pass
+            self._stop.wait(0.005)
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        self._stop.set()
+        if self._nv is not None:
+            self._t.join(timeout=1)
         if self.proc:
             self.proc.terminate()
             try:
@@ -87,6 +125,16 @@ class Clocks:
                 self.proc.kill()
 
     def summary(self):
+        if self._nv is not None and self.samples:
+            nv = self._nv
+            reasons = set()
+            for _, r in self.samples:
+                for name, attr in self.REASONS:
+                    if r & getattr(nv, attr, 0):
+                        reasons.add(name)
+            return {"sm_mhz": float(np.median([c for c, _ in self.samples])),
+                    "sm_max_mhz": self.smax, "reasons": sorted(reasons),
+                    "samples": len(self.samples), "source": "nvml 5 ms"}
         sm, smax, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
@@ -104,7 +152,7 @@ class Clocks:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": smax, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvidia-smi 200 ms"}
 
 
 def dist_env():
