@@ -780,9 +780,14 @@ __global__ void __launch_bounds__(kThreads) k_dense_tile(int n, int chunk,
     constexpr int CT = TC / 16;
     constexpr int NA = kGR * kGL / kThreads;  // A elements per thread per stage
     constexpr int NB = kGL * TC / kThreads;   // B elements per thread per stage
-    __shared__ double sA[kGL][kGR + 2];
-    __shared__ double sB[kGL][TC];
+    __shared__ __align__(16) double sA[kGL][kGR + 2];
+    __shared__ __align__(16) double sB[kGL][TC];
+    // thread (tx, ty) owns rows ty*8 .. ty*8+7 and, for even CT, the column
+    // pairs 2tx + 32q, 2tx + 32q + 1 (q < CT/2) so both fragments load as
+    // 128-bit shared-memory reads; odd CT keeps columns tx + 16c
+    constexpr bool PAIR = CT % 2 == 0;
     const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+    auto colof = [&](int c) { return PAIR ? 2 * tx + 32 * (c >> 1) + (c & 1) : tx + 16 * c; };
     const int i0 = blockIdx.x * kGR, j0 = blockIdx.y * TC, s = blockIdx.z;
     const int l0 = s * chunk, l1 = min(n, l0 + chunk);
     double acc[8][CT];
@@ -823,9 +828,22 @@ __global__ void __launch_bounds__(kThreads) k_dense_tile(int n, int chunk,
         for (int t = 0; t < tmax; ++t) {
             double a[8], bb[CT];
 #pragma unroll
-            for (int r = 0; r < 8; ++r) a[r] = sA[t][ty * 8 + r];
+            for (int r = 0; r < 8; r += 2) {
+                const double2 v = *reinterpret_cast<const double2*>(&sA[t][ty * 8 + r]);
+                a[r] = v.x;
+                a[r + 1] = v.y;
+            }
+            if constexpr (PAIR) {
 #pragma unroll
-            for (int c = 0; c < CT; ++c) bb[c] = sB[t][tx + 16 * c];
+                for (int c = 0; c < CT; c += 2) {
+                    const double2 v = *reinterpret_cast<const double2*>(&sB[t][colof(c)]);
+                    bb[c] = v.x;
+                    bb[c + 1] = v.y;
+                }
+            } else {
+#pragma unroll
+                for (int c = 0; c < CT; ++c) bb[c] = sB[t][colof(c)];
+            }
 #pragma unroll
             for (int r = 0; r < 8; ++r)
 #pragma unroll
@@ -838,7 +856,7 @@ __global__ void __launch_bounds__(kThreads) k_dense_tile(int n, int chunk,
         const int i = i0 + ty * 8 + r;
         if (i < n)
 #pragma unroll
-            for (int c = 0; c < CT; ++c) P[((size_t)s * n + i) * KC + j0 + tx + 16 * c] = acc[r][c];
+            for (int c = 0; c < CT; ++c) P[((size_t)s * n + i) * KC + j0 + colof(c)] = acc[r][c];
     }
 }
 
