@@ -2218,11 +2218,20 @@ extern "C" int cf_hier_create(int32_t nlev, const CfLevelDesc* ds, int32_t devic
             }
             if (d.kind == CF_LEVEL_AGGREGATION) {
                 l.ncolors = d.n_colors;
-                l.gs_classes = std::min(d.n_colors, kGsClasses);
-                l.merged = d.n_colors > kGsClasses;
+                static const int gs_env = [] {
+                    const char* e = std::getenv("CF_GS_CLASSES");
+                    return e ? std::max(0, std::atoi(e)) : kGsClasses;
+                }();
+                static const int gs_small = [] {  // levels below this many rows
+                    const char* e = std::getenv("CF_GS_SMALL_ROWS");
+                    return e ? std::atoi(e) : 0;
+                }();
+                const int gsk = d.n < gs_small ? 0 : gs_env;
+                l.gs_classes = std::min(d.n_colors, gsk);
+                l.merged = d.n_colors > gsk;
                 if (l.merged)
                     h->max_merged = std::max<int64_t>(
-                        h->max_merged, d.color_ptr[d.n_colors] - d.color_ptr[kGsClasses]);
+                        h->max_merged, d.color_ptr[d.n_colors] - d.color_ptr[l.gs_classes]);
                 l.cptr.assign(d.color_ptr, d.color_ptr + d.n_colors + 1);
                 l.crows = upload(*h, d.color_rows, (size_t)d.n);
                 l.contig = true;
@@ -2296,9 +2305,9 @@ extern "C" int cf_hier_create(int32_t nlev, const CfLevelDesc* ds, int32_t devic
                     l.c_nbr_lo.push_back(nbr_lo);
                 }
                 // distinct neighbour rows of the merged (Jacobi) classes, counted once
-                if (d.n_colors > kGsClasses) {
+                if (l.merged) {
                     std::vector<uint8_t> seen(d.n, 0);
-                    const int32_t mbeg = d.color_ptr[kGsClasses];
+                    const int32_t mbeg = d.color_ptr[l.gs_classes];
                     for (int32_t q = mbeg; q < d.color_ptr[d.n_colors]; ++q) {
                         int32_t i = d.color_rows[q];
                         for (int64_t p = d.rowptr[i]; p < d.rowptr[i + 1]; ++p) {
