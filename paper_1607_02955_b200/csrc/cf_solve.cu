@@ -425,8 +425,12 @@ __global__ void __launch_bounds__(kThreads) k_lincomb(int n, double* __restrict_
 // sequential sweep in colour order would use.  from_zero: x_i = b_i / L_ii.
 // Warps [0, cnt) take the class's rows (light rows only unless from_zero);
 // warps [cnt, cnt + nseg) take heavy-row segments (SegWork).
-template <int KC>
-__global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : kGatherCtas)) k_gs(const int32_t* __restrict__ rows,
+// SHORT (classes of short rows): CTAs take tiles of RPB x rpw rows, each warp
+// rpw rows through the row pipeline (next row's indices in flight), at 2
+// CTAs/SM so the pipeline state does not spill; heavy-row segment CTAs follow
+// the tiles.  Same per-row arithmetic as the warp-per-row form.
+template <int KC, bool SHORT = false>
+__global__ void __launch_bounds__(kThreads, SHORT ? 2 : (KC >= 256 ? 2 : kGatherCtas)) k_gs(const int32_t* __restrict__ rows,
                                                               int base, int cnt,
                                                               const int64_t* __restrict__ rp,
                                                               const int32_t* __restrict__ col,
@@ -434,15 +438,53 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : kGatherCtas)) k_gs(
                                                               const double* __restrict__ diag,
                                                               const double* __restrict__ B,
                                                               double* __restrict__ X,
-                                                              int from_zero, int jlim,
+                                                              int from_zero, int jlim, int rpw,
                                                               HeavyDev H, SegWork w) {
     CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
-    int64_t g = (int64_t)blockIdx.x * Lt::RPB + slot;
     if (!lane_ok) return;
-    int64_t i;
     DV<V> acc;
     zero(acc);
+    int64_t i;
+    int64_t g;
+    if constexpr (SHORT) {
+        const int64_t tile = (int64_t)Lt::RPB * rpw;
+        const int64_t ntile = ((int64_t)cnt + tile - 1) / tile;
+        if ((int64_t)blockIdx.x < ntile) {
+            const int64_t g0 = (int64_t)blockIdx.x * tile;
+            const int64_t gend = min((int64_t)cnt, g0 + tile);
+            auto row_of = [=](int64_t q) { return rows ? (int64_t)rows[q] : (int64_t)base + q; };
+            if (from_zero) {
+                for (int64_t q = g0 + slot; q < gend; q += Lt::RPB) {
+                    const int64_t r = row_of(q);
+                    DV<V> b = ldv<V>(B + r * KC + c0);
+                    const double d = diag[r];
+                    zero(acc);
+#pragma unroll
+                    for (int t = 0; t < V; ++t) acc.v[t] = (b.v[t] - acc.v[t]) / d;
+                    stv<V>(X + r * KC + c0, acc);
+                }
+                return;
+            }
+            row_pipeline<KC, G_PLAIN>(
+                g0 + slot, Lt::RPB, gend, row_of, rp, col, val, nullptr, nullptr,
+                [&](int64_t, int64_t r, int64_t beg, int64_t end, int jj, double aa, double dd) {
+                    if (H.hv && end - beg > kHeavyNnz) return;  // finished by its last segment warp
+                    DV<V> b = ldv<V>(B + r * KC + c0);
+                    const double d = diag[r];
+                    zero(acc);
+                    gather_row_from<KC, G_PLAIN>(col, val, beg, end, nullptr, nullptr, X, c0, acc,
+                                                 jj, aa, dd, jlim);
+#pragma unroll
+                    for (int t = 0; t < V; ++t) acc.v[t] = (b.v[t] - acc.v[t]) / d;
+                    stv<V>(X + r * KC + c0, acc);
+                });
+            return;
+        }
+        g = (int64_t)cnt + ((int64_t)blockIdx.x - ntile) * Lt::RPB + slot;
+    } else {
+        g = (int64_t)blockIdx.x * Lt::RPB + slot;
+    }
     if (g < cnt) {
         i = rows ? (int64_t)rows[g] : base + g;
         if (!from_zero) {
@@ -457,10 +499,10 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : kGatherCtas)) k_gs(
             return;
         }
     } else {
-        int64_t s = w.s_lo + (g - cnt);
-        if (s >= w.s_hi) return;
+        int64_t sg = w.s_lo + (g - cnt);
+        if (sg >= w.s_hi) return;
         int hv;
-        if (!seg_item<KC>(w, s, col, val, X, c0, hv, acc, jlim)) return;
+        if (!seg_item<KC>(w, sg, col, val, X, c0, hv, acc, jlim)) return;
         i = w.h_row[hv];
     }
     DV<V> b = ldv<V>(B + i * KC + c0);
@@ -473,19 +515,44 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : kGatherCtas)) k_gs(
 // Merged trailing colour classes, one Jacobi step: T[q] = (b_i - sum_j L_ij x_j) / L_ii
 // for i = rows[q] with every x_j read before any row of the step is written
 // (k_scatter_rows then writes T back).  Heavy rows as in k_gs.
-template <int KC>
-__global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : kGatherCtas)) k_jacobi_rows(
+template <int KC, bool SHORT = false>
+__global__ void __launch_bounds__(kThreads, SHORT ? 2 : (KC >= 256 ? 2 : kGatherCtas)) k_jacobi_rows(
     const int32_t* __restrict__ rows, int base, int cnt, const int64_t* __restrict__ rp,
     const int32_t* __restrict__ col, const double* __restrict__ val,
     const double* __restrict__ diag, const double* __restrict__ B, const double* __restrict__ X,
-    double* __restrict__ T, int jlim, HeavyDev H, SegWork w) {
+    double* __restrict__ T, int jlim, int rpw, HeavyDev H, SegWork w) {
     CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
-    int64_t g = (int64_t)blockIdx.x * Lt::RPB + slot;
     if (!lane_ok) return;
-    int64_t i, q;
+    int64_t i, q, g;
     DV<V> acc;
     zero(acc);
+    if constexpr (SHORT) {
+        const int64_t tile = (int64_t)Lt::RPB * rpw;
+        const int64_t ntile = ((int64_t)cnt + tile - 1) / tile;
+        if ((int64_t)blockIdx.x < ntile) {
+            const int64_t g0 = (int64_t)blockIdx.x * tile;
+            const int64_t gend = min((int64_t)cnt, g0 + tile);
+            auto row_of = [=](int64_t t) { return rows ? (int64_t)rows[t] : (int64_t)base + t; };
+            row_pipeline<KC, G_PLAIN>(
+                g0 + slot, Lt::RPB, gend, row_of, rp, col, val, nullptr, nullptr,
+                [&](int64_t qq, int64_t r, int64_t beg, int64_t end, int jj, double aa, double dd) {
+                    if (H.hv && end - beg > kHeavyNnz) return;
+                    DV<V> b = ldv<V>(B + r * KC + c0);
+                    const double d = diag[r];
+                    zero(acc);
+                    gather_row_from<KC, G_PLAIN>(col, val, beg, end, nullptr, nullptr, X, c0, acc,
+                                                 jj, aa, dd, jlim);
+#pragma unroll
+                    for (int t = 0; t < V; ++t) acc.v[t] = (b.v[t] - acc.v[t]) / d;
+                    stv<V>(T + qq * KC + c0, acc);
+                });
+            return;
+        }
+        g = (int64_t)cnt + ((int64_t)blockIdx.x - ntile) * Lt::RPB + slot;
+    } else {
+        g = (int64_t)blockIdx.x * Lt::RPB + slot;
+    }
     if (g < cnt) {
         i = rows ? (int64_t)rows[g] : base + g;
         q = g;
@@ -499,10 +566,10 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : kGatherCtas)) k_jac
         stv<V>(T + q * KC + c0, acc);
         return;
     }
-    int64_t s = w.s_lo + (g - cnt);
-    if (s >= w.s_hi) return;
+    int64_t sg = w.s_lo + (g - cnt);
+    if (sg >= w.s_hi) return;
     int hv;
-    if (!seg_item<KC>(w, s, col, val, X, c0, hv, acc, jlim)) return;
+    if (!seg_item<KC>(w, sg, col, val, X, c0, hv, acc, jlim)) return;
     i = w.h_row[hv];
     q = w.h_pos[hv] - base;
     DV<V> b = ldv<V>(B + i * KC + c0);
@@ -952,6 +1019,22 @@ static inline unsigned grid_tiles(int64_t rows, int64_t at_least = 1, int rpw = 
 #ifndef CF_RPW_MAX
 #define CF_RPW_MAX 8
 #endif
+// Short-row classes (mean off-degree <= CF_SHORT_DEG) with enough rows for
+// several per warp use the tiled sweep kernels at 2 CTAs/SM; 0 = warp per row.
+#ifndef CF_SHORT_DEG
+#define CF_SHORT_DEG 12
+#endif
+static inline int short_rpw(int64_t rows, int64_t nnz) {
+    static const int deg = [] {
+        const char* e = std::getenv("CF_SHORT_DEG");
+        return e ? std::atoi(e) : CF_SHORT_DEG;
+    }();
+    if (rows <= 0 || nnz > (int64_t)deg * rows) return 1;
+    // 4 rows per warp and still >= 4 waves of 2-CTA slots, else warp per row
+    // (measured: 2 rows per warp on C2's 20-30k-row classes is slower)
+    constexpr int64_t kSlots = 148 * 2 * kWarps, kWaves = 4;
+    return rows >= kSlots * kWaves * 4 ? 4 : 1;
+}
 static inline int pick_rpw(int64_t rows) {
     constexpr int64_t kSlots = 148 * 3 * kWarps, kWaves = 4;
     int r = CF_RPW_MAX;
@@ -1172,9 +1255,18 @@ struct Ops {
         const int64_t gnbr = from_zero ? 0 : first ? l.c_nbr_lo[colr] : l.c_nbr[colr];
         ProfScope ps(h, "gs_sweep", lev, 12.0 * l.c_nnz[colr] + 20.0 * cnt + Vb(2 * cnt + gnbr),
                      Vb(gnnz));
-        launch_k(k_gs<KC>, dim3(grid_rows<KC>(cnt + (w.s_hi - w.s_lo))), dim3(kThreads), 0, h.s,
-                 l.contig ? nullptr : l.crows + beg, beg, cnt, l.rp, l.col, l.val, l.diag, b, x,
-                 from_zero ? 1 : 0, first ? beg : 0x7fffffff, hd(h, l.pm), w);
+        const int rpw = short_rpw(cnt, l.c_nnz[colr]);
+        if (rpw > 1)
+            launch_k(k_gs<KC, true>,
+                     dim3(grid_tiles(cnt, 1, rpw) + grid_rows<KC>(w.s_hi - w.s_lo, 0)),
+                     dim3(kThreads), 0, h.s, l.contig ? nullptr : l.crows + beg, beg, cnt, l.rp,
+                     l.col, l.val, l.diag, b, x, from_zero ? 1 : 0, first ? beg : 0x7fffffff,
+                     rpw, hd(h, l.pm), w);
+        else
+            launch_k(k_gs<KC, false>, dim3(grid_rows<KC>(cnt + (w.s_hi - w.s_lo))),
+                     dim3(kThreads), 0, h.s, l.contig ? nullptr : l.crows + beg, beg, cnt, l.rp,
+                     l.col, l.val, l.diag, b, x, from_zero ? 1 : 0, first ? beg : 0x7fffffff, 1,
+                     hd(h, l.pm), w);
     }
 
     static void jacobi(Hier& h, DLevel& l, const double* b, double* x, bool first) {
@@ -1190,9 +1282,18 @@ struct Ops {
         {
             ProfScope ps(h, "jacobi_merged", lev, 12.0 * nnz + 20.0 * cnt + Vb(2 * cnt + gnbr),
                          Vb(gnnz));
-            launch_k(k_jacobi_rows<KC>, dim3(grid_rows<KC>(cnt + (w.s_hi - w.s_lo))), dim3(kThreads), 0, h.s,
-                     l.contig ? nullptr : l.crows + beg, beg, cnt, l.rp, l.col, l.val, l.diag, b,
-                     x, h.T, first ? beg : 0x7fffffff, hd(h, l.pm), w);
+            const int rpw = short_rpw(cnt, nnz);
+            if (rpw > 1)
+                launch_k(k_jacobi_rows<KC, true>,
+                         dim3(grid_tiles(cnt, 1, rpw) + grid_rows<KC>(w.s_hi - w.s_lo, 0)),
+                         dim3(kThreads), 0, h.s, l.contig ? nullptr : l.crows + beg, beg, cnt,
+                         l.rp, l.col, l.val, l.diag, b, x, h.T, first ? beg : 0x7fffffff, rpw,
+                         hd(h, l.pm), w);
+            else
+                launch_k(k_jacobi_rows<KC, false>, dim3(grid_rows<KC>(cnt + (w.s_hi - w.s_lo))),
+                         dim3(kThreads), 0, h.s, l.contig ? nullptr : l.crows + beg, beg, cnt,
+                         l.rp, l.col, l.val, l.diag, b, x, h.T, first ? beg : 0x7fffffff, 1,
+                         hd(h, l.pm), w);
         }
         ProfScope ps(h, "jacobi_scatter", lev, Vb(2 * cnt) + 4.0 * cnt);
         launch_k(k_scatter_rows<KC>, dim3(grid_rows<KC>(cnt)), dim3(kThreads), 0, h.s, 
