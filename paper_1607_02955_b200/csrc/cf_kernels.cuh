@@ -60,7 +60,7 @@ inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sme
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 #ifndef CF_ROWS_PER_PART
-#define CF_ROWS_PER_PART 64
+#define CF_ROWS_PER_PART 32
 #endif
 constexpr int kRowsPerPart = CF_ROWS_PER_PART;
 #ifndef CF_GATHER_CTAS
