@@ -836,14 +836,24 @@ __global__ void __launch_bounds__(kThreads) k_dense_small(int n, int chunk,
 // stages in shared memory, 8 x (TC/16) register tile per thread; the next
 // stage's tiles are prefetched into registers while the current one is
 // multiplied (global-load latency overlapped with the fp64 FMAs).
-constexpr int kGR = 128, kGL = 16;
+// Column-tile width (experiment knob; every output keeps its fma chain, so
+// results do not depend on it).  64 (8 x 4 thread tile, 128 registers, 2
+// CTAs/SM) was measured against 128 (8 x 8, 246 registers, 1 CTA/SM): C2
+// 12.24 vs 12.07 ms per step, dense share 7.0 vs 6.0 % (profiles/r01/
+// dense_tile_ab.txt), so the wider tile stays.
+#ifndef CF_DENSE_TC
+#define CF_DENSE_TC 128
+#endif
+constexpr int kGR = 128, kGL = 16, kDenseTC = CF_DENSE_TC;
+template <int KC>
+constexpr int dense_tc() { return KC < kDenseTC ? KC : kDenseTC; }
 template <int KC>
 __global__ void __launch_bounds__(kThreads) k_dense_tile(int n, int chunk,
                                                          const double* __restrict__ M,
                                                          const double* __restrict__ B,
                                                          double* __restrict__ P) {
     CF_PDL_ENTRY();
-    constexpr int TC = KC < 128 ? KC : 128;
+    constexpr int TC = dense_tc<KC>();
     constexpr int CT = TC / 16;
     constexpr int NA = kGR * kGL / kThreads;  // A elements per thread per stage
     constexpr int NB = kGL * TC / kThreads;   // B elements per thread per stage
@@ -1165,7 +1175,7 @@ struct Ops {
                 ProfScope ps(h, "dense", j, 8.0 * l.n * l.n + 2 * Vb(l.n));
                 const int S = dense_splits(l.n), chunk = dense_chunk(l.n, S);
                 if constexpr (KC >= 16) {
-                    dim3 grd((unsigned)((l.n + kGR - 1) / kGR), KC / (KC < 128 ? KC : 128), S);
+                    dim3 grd((unsigned)((l.n + kGR - 1) / kGR), KC / dense_tc<KC>(), S);
                     launch_k(k_dense_tile<KC>, dim3(grd), dim3(kThreads), 0, h.s, l.n, chunk, l.M, b, h.DP);
                 } else {
                     dim3 grd((unsigned)(((int64_t)l.n * KC + kThreads - 1) / kThreads), S);
