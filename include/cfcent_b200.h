@@ -152,10 +152,16 @@ int cf_jl_rhs_rows(void* graph, uint64_t state_hi, uint64_t state_lo, uint64_t i
 int cf_jl_sketch(void* graph, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
                  uint64_t inc_lo, int64_t K, int64_t row0, int64_t n_rows, double inv_sqrt_k,
                  const int64_t* query, int64_t n_query, const CfSolveParams* params,
-                 double* out_sums, double* z_rows, double* residuals, CfSolveStats* stats);
+                 double* out_sums, double* row_parts, double* z_rows, double* residuals,
+                 CfSolveStats* stats);
 /* (cf_jl_sketch computes sketch rows [row0, row0 + n_rows) of the K-row
- * sketch; out_sums are the additive contributions of those rows, so ranks
- * owning disjoint row ranges sum their outputs -- SURVEY.md §8(e).) */
+ * sketch; out_sums are the contributions of those rows.  If row_parts is not
+ * NULL it receives, per row j, [T_j, C_j, Z[q_0, j], ..., Z[q_{nq-1}, j]]
+ * (n_rows x (2 + n_query) host): ranks owning disjoint row ranges gather
+ * their row parts and cf_jl_combine sums them in ascending row order, which
+ * gives the same bits for every split -- SURVEY.md §8(e).) */
+int cf_jl_combine(const double* row_parts, int64_t n_rows, int64_t n_query, int64_t n,
+                  double* out_sums);
 
 /* Amortised node solutions L z_x = e_x - 1/n (resistance.py:77-99) for the
  * given nodes, reduced on device to the |nodes| x |nodes| submatrix

@@ -83,8 +83,9 @@ _SIGS = {
                                  C.c_int64, C.c_int64, C.c_int32, f64p]),
     "cf_jl_sketch": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
                                C.c_int64, C.c_int64, C.c_int64, C.c_double, i64p, C.c_int64,
-                               C.POINTER(CfSolveParams), f64p, f64p, f64p,
+                               C.POINTER(CfSolveParams), f64p, f64p, f64p, f64p,
                                C.POINTER(CfSolveStats)]),
+    "cf_jl_combine": (C.c_int, [f64p, C.c_int64, C.c_int64, C.c_int64, f64p]),
     "cf_node_solutions": (C.c_int, [C.c_void_p, i64p, C.c_int64, C.POINTER(CfSolveParams), f64p,
                                     f64p, f64p, C.POINTER(CfSolveStats)]),
     "cf_hier_stream": (C.c_void_p, [C.c_void_p]),

@@ -207,9 +207,9 @@ def _pcg_words(seed: int):
 
 def _sketch_device(g: Graph, hierarchy: MultigridHierarchy, epsilon: float, seed: int,
                    config: SolverConfig, query: np.ndarray | None, want_z: bool,
-                   rows: tuple[int, int] | None = None):
+                   rows: tuple[int, int] | None = None, want_parts: bool = False):
     """Device JL sketch of rows [r0, r1) (all k rows by default).  Returns
-    (k, z rows|None, additive per-query sums over those rows, residuals)."""
+    (k, z rows|None, per-query sums over those rows, residuals[, row parts])."""
     if not 0 < epsilon <= 1:
         raise DomainError(f"epsilon must be in (0, 1], got {epsilon}")
     n = g.n
@@ -221,15 +221,18 @@ def _sketch_device(g: Graph, hierarchy: MultigridHierarchy, epsilon: float, seed
     q = np.zeros(0, dtype=np.int64) if query is None else np.asarray(query, np.int64)
     q = np.ascontiguousarray(hierarchy.device().inv0[q], dtype=np.int64)
     sums = np.zeros(max(q.size, 1))
+    parts = np.empty((r1 - r0, 2 + q.size)) if want_parts else None
     z = np.empty((r1 - r0, n)) if want_z else None
     res = np.zeros(r1 - r0)
     st = N.CfSolveStats()
     sh, sl, ih, il = _pcg_words(seed)
     N.check(N.lib().cf_jl_sketch(dg.handle, sh, sl, ih, il, k, r0, r1 - r0, 1.0 / math.sqrt(k),
                                  N.ptr(q, N.i64p), q.size, N.C.byref(_params(config, n)),
-                                 N.ptr(sums, N.f64p), N.ptr(z, N.f64p), N.ptr(res, N.f64p),
-                                 N.C.byref(st)), st)
+                                 N.ptr(sums, N.f64p), N.ptr(parts, N.f64p), N.ptr(z, N.f64p),
+                                 N.ptr(res, N.f64p), N.C.byref(st)), st)
     hierarchy.stats.record(res, int(st.fallback_solves), int(st.vcycles))
+    if want_parts:
+        return k, z, sums[:q.size], res, parts
     return k, z, sums[:q.size], res
 
 
@@ -259,14 +262,30 @@ def jl_rhs_rows(g: Graph, hierarchy: MultigridHierarchy, k: int, seed: int, row0
 
 def sketch_closeness_sums(g: Graph, hierarchy: MultigridHierarchy, epsilon: float, seed: int,
                           query: Sequence[int], config: SolverConfig | None = None,
-                          rows: tuple[int, int] | None = None):
+                          rows: tuple[int, int] | None = None, row_parts: bool = False):
     """Fused device JL path: returns (k, sums_v for query, residuals).  With
     ``rows`` only that range of sketch rows is solved and the sums are its
-    additive share (multi-GPU sharding)."""
+    share.  With ``row_parts`` a fourth value is returned: the per-row parts
+    [T_j, C_j, Z[q, j]...] ((r1 - r0) x (2 + |query|)) that ``combine_row_parts``
+    sums in row order -- bitwise the same total for any split of the rows over
+    ranks (multi-GPU sharding)."""
     config = config or hierarchy.config
-    k, _, sums, res = _sketch_device(g, hierarchy, epsilon, seed, config,
-                                     np.asarray(query, dtype=np.int64), False, rows)
-    return k, sums, res
+    out = _sketch_device(g, hierarchy, epsilon, seed, config,
+                         np.asarray(query, dtype=np.int64), False, rows, row_parts)
+    return out[0], out[2], out[3], *out[4:]
+
+
+def combine_row_parts(parts: np.ndarray, n: int) -> np.ndarray:
+    """sum_w ||z_v - z_w||^2 for the query nodes from per-row parts stacked in
+    ascending sketch-row order (cf_jl_combine; resistance.py:218-237)."""
+    parts = np.ascontiguousarray(parts, dtype=np.float64)
+    if parts.ndim != 2 or parts.shape[1] < 2:
+        raise DomainError("row parts must be (rows, 2 + |query|)")
+    nq = parts.shape[1] - 2
+    out = np.zeros(max(nq, 1))
+    N.check(N.lib().cf_jl_combine(N.ptr(parts, N.f64p), parts.shape[0], nq, int(n),
+                                  N.ptr(out, N.f64p)))
+    return out[:nq]
 
 
 def sketch_distance(sketch: ResistanceSketch, u: int, v: int) -> float:

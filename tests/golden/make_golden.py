@@ -225,6 +225,132 @@ def config3(tau_list=(1e-6, 1e-10)):
         save("config3.npz", **d)
 
 
+def _rmat_reference_graph(scale, edge_factor, seed, weighted):
+    """R-MAT recipe of SURVEY.md §8(d) (frozen in paper_1607_02955_b200/
+    configs.py:rmat_graph), restated here on the reference's own Graph and
+    largest_connected_component (graph.py:100-147, 217-250)."""
+    rng = np.random.default_rng(seed)
+    n = 1 << scale
+    M = edge_factor * n
+    a, b, c = 0.57, 0.19, 0.19
+    u = np.zeros(M, dtype=np.int64)
+    v = np.zeros(M, dtype=np.int64)
+    for bit in range(scale):
+        r = rng.random(M)
+        u |= (r >= a + b).astype(np.int64) << bit
+        v |= (((r >= a) & (r < a + b)) | (r >= a + b + c)).astype(np.int64) << bit
+    keep = u != v
+    lo = np.minimum(u[keep], v[keep])
+    hi = np.maximum(u[keep], v[keep])
+    key = np.unique(lo * n + hi)
+    lo, hi = key // n, key % n
+    w = (2.0 - rng.random(lo.size) * 1.5) if weighted else np.ones(lo.size)
+    g = cfcent.Graph.from_edges(lo, hi, w, n=n)
+    return cfcent.largest_connected_component(g)[0]
+
+
+def _jl_rows_reference(g, h, k, seed, rows, cfg):
+    """Rows [0, rows) of the reference sketch (resistance.py:177-201): the
+    first rows*m draws of default_rng(seed).integers(0, 2) are the first
+    ``rows`` rows of the full k x m Q (row-major stream), scaled
+    by 1/sqrt(k) of the FULL k; right-hand sides centred and solved by the
+    reference's solve_many."""
+    b_inc, weights = cfcent.incidence_and_weights(g)
+    scaled_t = b_inc.multiply(np.sqrt(weights)[:, None]).T.tocsr()
+    rng = np.random.default_rng(seed)
+    q = (rng.integers(0, 2, size=(rows, g.m)).astype(np.float64) * 2.0 - 1.0) / math.sqrt(k)
+    rhs = (scaled_t @ q.T).T
+    rhs -= rhs.mean(axis=1, keepdims=True)
+    solved = slv.solve_many(h, rhs, cfg)
+    z = np.vstack([p.values for p in solved])
+    res_ = np.array([p.achieved_residual for p in solved])
+    return z, res_
+
+
+def _partial_sums(z, nodes):
+    """Additive share of sketch_distance_sums (resistance.py:218-237) over
+    the sketch rows held in z."""
+    col_sq = np.einsum("ij,ij->j", z, z)
+    return col_sq.sum() + z.shape[1] * col_sq[nodes] - 2.0 * (z[:, nodes].T @ z.sum(axis=1))
+
+
+def _cpu_info():
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return f"{model}; {os.cpu_count()} cores"
+
+
+def config_rmat(name, scale, ef, seed, weighted, k, query_fn, jl_rows=32, samp=None,
+                tau_list=(1e-6, 1e-10)):
+    """C4/C5 reference goldens: JL partial sums over sketch rows [0, jl_rows)
+    at each tau, and (C5) amortised resistances R(u, t) for the first pivots
+    of the sampling pivot set.  The reference setup on these graphs takes
+    tens of minutes to hours (831+ levels); timings are recorded as the cached
+    CPU baseline (provenance: this container)."""
+    path = os.path.join(OUT, f"{name}.npz")
+    d = {}
+    if os.path.exists(path):
+        with np.load(path, allow_pickle=True) as prev:
+            d.update({kk: prev[kk] for kk in prev.files if kk != "provenance"})
+    t0 = time.perf_counter()
+    g = _rmat_reference_graph(scale, ef, seed, weighted)
+    t1 = time.perf_counter()
+    query = np.asarray(query_fn(g), dtype=np.int64)
+    d.update({"n": np.int64(g.n), "m": np.int64(g.m), "query": query, "k": np.int64(k),
+              "jl_rows": np.int64(jl_rows), "t_graph": np.float64(t1 - t0),
+              "cpu": np.array(_cpu_info())})
+    print(name, "graph", g.n, g.m, t1 - t0, flush=True)
+    cfg0 = slv.SolverConfig(tau=tau_list[0], seed=0)
+    h = slv.setup(cfcent.laplacian(g), cfg0)
+    t2 = time.perf_counter()
+    d["sizes"] = np.array(h.level_sizes)
+    d["t_setup"] = np.float64(t2 - t1)
+    print(name, "setup", len(h.level_sizes), "levels", t2 - t1, flush=True)
+    save(f"{name}.npz", **d)
+    for tau in tau_list:
+        cfg = slv.SolverConfig(tau=tau, seed=0)
+        tag = f"{tau:.0e}".replace("-", "m")
+        t3 = time.perf_counter()
+        z, r = _jl_rows_reference(g, h, k, 0, jl_rows, cfg)
+        t4 = time.perf_counter()
+        d[f"jl_psum_{tag}"] = _partial_sums(z, query)
+        d[f"jl_res_{tag}"] = r
+        d[f"t_jl_{tag}"] = np.float64(t4 - t3)
+        print(name, tau, "jl", d[f"jl_psum_{tag}"][:3], t4 - t3, flush=True)
+        save(f"{name}.npz", **d)
+        if samp is not None:
+            npiv, pseed, cnt = samp
+            u = int(query[0])
+            piv = cfcent.centrality.pivot_set(g.n, npiv, pseed)[:cnt]
+            t5 = time.perf_counter()
+            rr = res.resistances_from_node(h, u, piv, cfg, cache={}, threads=2)
+            t6 = time.perf_counter()
+            d["samp_pivots"] = piv
+            d[f"samp_r_{tag}"] = rr
+            d[f"t_samp_{tag}"] = np.float64(t6 - t5)
+            print(name, tau, "samp", rr[:3], t6 - t5, flush=True)
+            save(f"{name}.npz", **d)
+
+
+def config4():
+    config_rmat("config4", 20, 16, 4, True, 256,
+                lambda g: np.sort(np.random.default_rng(4).choice(g.n, 1000, replace=False)))
+
+
+def config5():
+    def q(g):
+        return np.array([int(np.argmax(np.diff(g.indptr)))])
+    n_est = 2234040
+    k = math.ceil(4 * math.log(n_est) / 0.09)
+    config_rmat("config5", 22, 12, 5, False, k, q, samp=(1024, 5, 64))
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["kats", "small", "c1", "c2"]
     if "kats" in which:
@@ -237,5 +363,9 @@ if __name__ == "__main__":
         config2()
     if "c3" in which:
         config3()
+    if "c4" in which:
+        config4()
+    if "c5" in which:
+        config5()
     if "c3tau10" in which:  # the tau_parity values alone (~2 h of reference CPU time)
         config3((1e-10,))

@@ -175,9 +175,15 @@ def test_config3_properties():
     eps = math.sqrt(math.log(bc.graph.n) / (bc.jl_k - 0.5))
     k, full, res = sketch_closeness_sums(bc.graph, h, eps, 0, bc.query, cfg)
     assert k == 128 and res.max() <= bc.tau
-    _, a, _ = sketch_closeness_sums(bc.graph, h, eps, 0, bc.query, cfg, rows=(0, 50))
-    _, b, _ = sketch_closeness_sums(bc.graph, h, eps, 0, bc.query, cfg, rows=(50, 128))
+    # strong multi-GPU split (distributed.py): row parts of two ranges stacked
+    # in row order and combined give the single run's sums BITWISE
+    from paper_1607_02955_b200.resistance import combine_row_parts
+    _, a, _, pa = sketch_closeness_sums(bc.graph, h, eps, 0, bc.query, cfg, rows=(0, 50),
+                                        row_parts=True)
+    _, b, _, pb = sketch_closeness_sums(bc.graph, h, eps, 0, bc.query, cfg, rows=(50, 128),
+                                        row_parts=True)
     assert np.allclose(a + b, full, rtol=1e-10)
+    assert combine_row_parts(np.concatenate([pa, pb]), bc.graph.n).tobytes() == full.tobytes()
     lap = P.laplacian(bc.graph)
     rng = np.random.default_rng(3)
     s = rng.standard_normal((3, bc.graph.n))

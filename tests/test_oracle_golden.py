@@ -85,3 +85,21 @@ def test_config1_hierarchy_rhs_and_scores():
     exact_jl = O.jl_exact_pinv(g, k, 0, q)
     assert np.allclose(d["jl_1em10"], exact_jl, rtol=1e-8)
     assert np.allclose(d["jl_1em08"], exact_jl, rtol=1e-6)
+
+
+def test_workload_graphs_match_product_generators():
+    """bench.py's CPU reference arm builds its input with oracle/workloads.py
+    (no product code); the product arm with paper_1607_02955_b200/configs.py.
+    Same recipe, same draws -> the same graph (small R-MAT / RGG / C1 / C2)."""
+    from oracle import workloads as OW
+    from paper_1607_02955_b200 import configs
+    for og, pg in ((OW.rmat_graph(12, 8, 4, True), configs.rmat_graph(12, 8, 4, weighted=True)),
+                   (OW.rmat_graph(11, 12, 5, False), configs.rmat_graph(11, 12, 5, weighted=False)),
+                   (OW.rgg_graph(5000, 3), configs.rgg_graph(5000, 3)),
+                   (OW.make("c1")["graph"], configs.make("c1").graph)):
+        assert np.array_equal(og[0], pg.indptr)
+        assert np.array_equal(og[1], pg.indices)
+        assert np.array_equal(og[2], pg.weights)
+    wl, bc = OW.make("c2"), configs.make("c2")
+    assert np.array_equal(wl["graph"][1], bc.graph.indices)
+    assert np.array_equal(wl["query"], bc.query)
