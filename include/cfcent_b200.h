@@ -91,6 +91,10 @@ typedef struct {
     int64_t outer_iterations;    /* block iterations executed */
     double max_residual;
     double best_residual;        /* on CF_CONVERGENCE: worst failing residual */
+    int64_t krylov_solves;       /* columns continued under V-cycle-preconditioned FCG
+                                    by the Krylov hand-off; NOT
+                                    counted in fallback_solves, which keeps the
+                                    reference meaning (solver.py:717-720) */
 } CfSolveStats;
 
 const char* cf_last_error(void);
@@ -118,15 +122,19 @@ int cf_solve_rows(void* handle, const double* supplies_rows, int64_t count,
                   const CfSolveParams* params, double* values_rows,
                   double* residuals, CfSolveStats* stats);
 
-/* Same on device memory: B_dev, X_dev are n x k row-major (k <= 256). */
+/* Same on device memory: B_dev, X_dev are n x k row-major (k <= 256).
+ * caller_stream (a cudaStream_t, NULL = legacy default stream) is the stream
+ * that produced B_dev: the library's stream waits on it (event) before reading
+ * the inputs; outputs are complete when the call returns. */
 int cf_solve_block_dev(void* handle, const double* B_dev, double* X_dev, int32_t k,
                        const CfSolveParams* params, double* residuals,
-                       CfSolveStats* stats);
+                       CfSolveStats* stats, void* caller_stream);
 
 /* Exported for unit tests: R = B - L X and per-column sum(R^2) on level 0
- * (solver.py:694-695). Device pointers, n x k row-major. */
+ * (solver.py:694-695). Device pointers, n x k row-major; caller_stream as for
+ * cf_solve_block_dev. */
 int cf_residual_dev(void* handle, const double* B_dev, const double* X_dev, double* R_dev,
-                    int32_t k, double* colsq_host);
+                    int32_t k, double* colsq_host, void* caller_stream);
 
 /* --- estimators (resistance.py / centrality.py) ----------------------- */
 /* Graph upload for the JL right-hand sides: adjacency (graph.py:30-98) with
@@ -171,6 +179,15 @@ int cf_jl_combine(const double* row_parts, int64_t n_rows, int64_t n_query, int6
 int cf_node_solutions(void* handle, const int64_t* nodes, int64_t cnt,
                       const CfSolveParams* params, double* sub, double* z_rows,
                       double* residuals, CfSolveStats* stats);
+
+/* Exact current-flow closeness denominators (centrality.py:78-101): every node
+ * is solved once (L z_t = e_t - 1/n, resistance.py:77-99) and, per query v
+ * (device-order node ids), S_v = sum_t R(v, t) is accumulated on the device
+ * without returning the n x n solutions.  max_residual (host, may be NULL)
+ * receives the largest relative residual of the n solves. */
+int cf_exact_sums(void* handle, const int64_t* query, int64_t n_query,
+                  const CfSolveParams* params, double* out_sums, double* max_residual,
+                  CfSolveStats* stats);
 
 /* --- measurement ------------------------------------------------------- */
 /* the cudaStream_t every kernel of this hierarchy is launched on */

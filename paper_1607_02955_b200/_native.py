@@ -54,7 +54,7 @@ class CfSolveStats(C.Structure):
     _fields_ = [
         ("solves", C.c_int64), ("fallback_solves", C.c_int64), ("vcycles", C.c_int64),
         ("outer_iterations", C.c_int64), ("max_residual", C.c_double),
-        ("best_residual", C.c_double),
+        ("best_residual", C.c_double), ("krylov_solves", C.c_int64),
     ]
 
 
@@ -73,9 +73,10 @@ _SIGS = {
     "cf_solve_rows": (C.c_int, [C.c_void_p, f64p, C.c_int64, C.POINTER(CfSolveParams), f64p,
                                 f64p, C.POINTER(CfSolveStats)]),
     "cf_solve_block_dev": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
-                                     C.POINTER(CfSolveParams), f64p, C.POINTER(CfSolveStats)]),
+                                     C.POINTER(CfSolveParams), f64p, C.POINTER(CfSolveStats),
+                                     C.c_void_p]),
     "cf_residual_dev": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
-                                  f64p]),
+                                  f64p, C.c_void_p]),
     "cf_graph_create": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, i64p, i32p, i32p, f64p,
                                   C.POINTER(C.c_void_p)]),
     "cf_graph_destroy": (C.c_int, [C.c_void_p]),
@@ -88,6 +89,8 @@ _SIGS = {
     "cf_jl_combine": (C.c_int, [f64p, C.c_int64, C.c_int64, C.c_int64, f64p]),
     "cf_node_solutions": (C.c_int, [C.c_void_p, i64p, C.c_int64, C.POINTER(CfSolveParams), f64p,
                                     f64p, f64p, C.POINTER(CfSolveStats)]),
+    "cf_exact_sums": (C.c_int, [C.c_void_p, i64p, C.c_int64, C.POINTER(CfSolveParams), f64p,
+                                f64p, C.POINTER(CfSolveStats)]),
     "cf_hier_stream": (C.c_void_p, [C.c_void_p]),
     "cf_profile": (C.c_int, [C.c_void_p, C.c_int32]),
     "cf_profile_report": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int64, i64p]),

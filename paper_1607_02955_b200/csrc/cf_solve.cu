@@ -1835,6 +1835,7 @@ static void solve_block_t(Hier& h, int ncols, const CfSolveParams& p, double* re
             if (any) {
                 int nk = 0;
                 for (int c = 0; c < KC; ++c) nk += kr[c];
+                st.krylov_solves += nk;
                 st.vcycles += O::krylov(h, p.nu1, p.nu2, std::max(1, p.max_cycles - kKrylovCheck),
                                         nk);
                 CF_CUDA(cudaMemcpyAsync(state.data(), h.state, sizeof(int) * KC,
@@ -2539,6 +2540,18 @@ extern "C" int cf_solve_rows(void* hp, const double* rows, int64_t count,
                                     cudaMemcpyHostToDevice, h.cs));
             CF_CUDA(cudaEventRecord(h.ev_in[q], h.cs));
         };
+        // an exception (unbalanced column, convergence failure) must not
+        // return while copies into / out of the caller's buffers are queued
+        struct Drain {
+            Hier& h;
+            bool armed = true;
+            ~Drain() {
+                if (armed) {
+                    cudaStreamSynchronize(h.s);
+                    cudaStreamSynchronize(h.cs);
+                }
+            }
+        } drain{h};
         issue_in(0);
         for (size_t b = 0; b < nb; ++b) {
             const int q = (int)(b & 1);
@@ -2557,6 +2570,7 @@ extern "C" int cf_solve_rows(void* hp, const double* rows, int64_t count,
             CF_CUDA(cudaEventRecord(h.ev_out_done[q], h.cs));
             std::memcpy(residuals + off[b], res.data(), sizeof(double) * num[b]);
         }
+        drain.armed = false;
         CF_CUDA(cudaStreamSynchronize(h.s));
         CF_CUDA(cudaStreamSynchronize(h.cs));
         done = count;
@@ -2578,12 +2592,25 @@ extern "C" int cf_solve_rows(void* hp, const double* rows, int64_t count,
     CF_API_END_STATS(st)
 }
 
+// The library stream h.s is a non-blocking stream: device inputs produced on
+// the caller's stream are ordered before this call's kernels by an event.
+static void order_after(Hier& h, void* caller_stream) {
+    cudaEvent_t ev;
+    CF_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    cudaError_t e1 = cudaEventRecord(ev, (cudaStream_t)caller_stream);
+    cudaError_t e2 = e1 == cudaSuccess ? cudaStreamWaitEvent(h.s, ev, 0) : e1;
+    cudaEventDestroy(ev);
+    CF_CUDA(e2);
+}
+
 extern "C" int cf_solve_block_dev(void* hp, const double* B_dev, double* X_dev, int32_t k,
-                                  const CfSolveParams* p, double* residuals, CfSolveStats* st) {
+                                  const CfSolveParams* p, double* residuals, CfSolveStats* st,
+                                  void* caller_stream) {
     CF_API_BEGIN
     Hier& h = *(Hier*)hp;
     std::lock_guard<std::mutex> lk(h.mu);
     CF_CUDA(cudaSetDevice(h.dev));
+    order_after(h, caller_stream);
     if (k < 1 || k > kMaxKC) throw CfError(CF_DOMAIN, "k must be in [1, 256]");
     int kc = kc_at_least(k);
     h.ensure_workspace(kc);
@@ -2602,11 +2629,12 @@ extern "C" int cf_solve_block_dev(void* hp, const double* B_dev, double* X_dev, 
 }
 
 extern "C" int cf_residual_dev(void* hp, const double* B_dev, const double* X_dev, double* R_dev,
-                               int32_t k, double* colsq) {
+                               int32_t k, double* colsq, void* caller_stream) {
     CF_API_BEGIN
     Hier& h = *(Hier*)hp;
     std::lock_guard<std::mutex> lk(h.mu);
     CF_CUDA(cudaSetDevice(h.dev));
+    order_after(h, caller_stream);
     int kc = kc_at_least(k);
     if (kc != k) throw CfError(CF_DOMAIN, "k must be a supported block width");
     h.ensure_workspace(kc);

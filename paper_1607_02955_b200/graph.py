@@ -22,7 +22,7 @@ from scipy.sparse.csgraph import connected_components
 
 from .errors import DomainError
 
-__all__ = ["Graph", "largest_connected_component", "laplacian", "incidence_and_weights",
+__all__ = ["Graph", "check_connected", "largest_connected_component", "laplacian", "incidence_and_weights",
            "edge_index_view"]
 
 
@@ -157,6 +157,18 @@ def largest_connected_component(g: Graph):
     sub = Graph.from_edges(remap[eu[sel]], remap[ev[sel]], ew[sel], n=keep.size,
                            node_labels=g.node_labels[keep].copy())
     return sub, {int(a): int(b) for a, b in zip(keep, remap[keep])}
+
+
+def check_connected(g: Graph) -> None:
+    """DomainError unless ``g`` is connected (graph.py:338-348); one
+    connected-components pass over the CSR adjacency."""
+    if g.n == 0:
+        raise DomainError("empty graph")
+    if g.n == 1:
+        return
+    ncomp, _ = connected_components(g.adjacency_matrix(), directed=False)
+    if ncomp != 1:
+        raise DomainError("graph is not connected; extract the LCC first")
 
 
 def laplacian(g: Graph) -> sp.csr_matrix:

@@ -68,10 +68,11 @@ def effective_resistance(hierarchy: MultigridHierarchy, u: int, v: int,
 def _node_solve(hierarchy: MultigridHierarchy, nodes: np.ndarray, config: SolverConfig,
                 full: bool):
     """Device solve of L z_x = e_x - 1/n for each x in ``nodes`` (sorted).
-    Returns (sub, z_rows|None, residuals): sub[a, b] = z_{nodes[a]}[nodes[b]]."""
+    Returns (sub|None, z_rows|None, residuals): sub[a, b] = z_{nodes[a]}[nodes[b]]
+    (only when the full solutions are not requested)."""
     n = hierarchy.n
     cnt = nodes.size
-    sub = np.empty((cnt, cnt))
+    sub = None if full else np.empty((cnt, cnt))
     z = np.empty((cnt, n)) if full else None
     res = np.zeros(cnt)
     if cnt == 0:
@@ -82,7 +83,8 @@ def _node_solve(hierarchy: MultigridHierarchy, nodes: np.ndarray, config: Solver
     N.check(N.lib().cf_node_solutions(dev.handle, N.ptr(nd, N.i64p), cnt,
                                       N.C.byref(_params(config, n)), N.ptr(sub, N.f64p),
                                       N.ptr(z, N.f64p), N.ptr(res, N.f64p), N.C.byref(st)), st)
-    hierarchy.stats.record(res, int(st.fallback_solves), int(st.vcycles))
+    hierarchy.stats.record(res, int(st.fallback_solves), int(st.vcycles),
+                           int(st.krylov_solves))
     return sub, z, res
 
 
@@ -230,7 +232,8 @@ def _sketch_device(g: Graph, hierarchy: MultigridHierarchy, epsilon: float, seed
                                  N.ptr(q, N.i64p), q.size, N.C.byref(_params(config, n)),
                                  N.ptr(sums, N.f64p), N.ptr(parts, N.f64p), N.ptr(z, N.f64p),
                                  N.ptr(res, N.f64p), N.C.byref(st)), st)
-    hierarchy.stats.record(res, int(st.fallback_solves), int(st.vcycles))
+    hierarchy.stats.record(res, int(st.fallback_solves), int(st.vcycles),
+                           int(st.krylov_solves))
     if want_parts:
         return k, z, sums[:q.size], res, parts
     return k, z, sums[:q.size], res

@@ -122,8 +122,10 @@ class LevelKind(Enum):
 
 @dataclass
 class Level:
-    """One hierarchy level (solver.py:97-120).  ``m_lower``/``m_upper`` are not
-    materialised: the device smoother uses ``colors`` (multicolour GS)."""
+    """One hierarchy level (solver.py:97-120).  ``m_lower``/``m_upper`` (the
+    reference's Gauss-Seidel triangles, solver.py:503-504) are built on first
+    access for aggregation levels and cached; the device smoother itself uses
+    ``colors`` (multicolour GS) and never needs them."""
 
     kind: LevelKind
     matrix: sp.csr_matrix
@@ -134,33 +136,56 @@ class Level:
     w_fc: sp.csr_matrix | None = None
     p: sp.csr_matrix | None = None
     aggregates: np.ndarray | None = None
-    m_lower: sp.csr_matrix | None = None
-    m_upper: sp.csr_matrix | None = None
     grounded_factor: tuple | None = None
     colors: np.ndarray | None = None
+    _tri: dict = field(default_factory=dict, repr=False, compare=False)
 
     @property
     def size(self) -> int:
         return self.matrix.shape[0]
 
+    def _triangle(self, which: str):
+        if self.kind is not LevelKind.AGGREGATION:
+            return None
+        t = self._tri.get(which)
+        if t is None:
+            t = (sp.tril if which == "lower" else sp.triu)(self.matrix, 0, format="csr")
+            self._tri[which] = t
+        return t
+
+    @property
+    def m_lower(self) -> sp.csr_matrix | None:
+        return self._triangle("lower")
+
+    @property
+    def m_upper(self) -> sp.csr_matrix | None:
+        return self._triangle("upper")
+
 
 @dataclass
 class SolveStats:
-    """solver.py:123-137, plus device counters."""
+    """solver.py:123-137, plus device counters.  ``fallback_solves`` keeps the
+    reference meaning (columns that entered the FCG fallback after the
+    stagnation rule, solver.py:717-720); ``krylov_solves`` counts columns the
+    Krylov hand-off continued under V-cycle-preconditioned
+    FCG before any stagnation."""
 
     solves: int = 0
     max_residual: float = 0.0
     fallback_solves: int = 0
     vcycles: int = 0
+    krylov_solves: int = 0
     _lock: threading.Lock = field(default_factory=threading.Lock, repr=False)
 
-    def record(self, residuals: np.ndarray, fallbacks: int, vcycles: int = 0) -> None:
+    def record(self, residuals: np.ndarray, fallbacks: int, vcycles: int = 0,
+               krylov: int = 0) -> None:
         with self._lock:
             self.solves += residuals.size
             if residuals.size:
                 self.max_residual = max(self.max_residual, float(residuals.max()))
             self.fallback_solves += fallbacks
             self.vcycles += vcycles
+            self.krylov_solves += krylov
 
 
 _DEVICE: int | None = None
@@ -725,8 +750,8 @@ def setup(matrix: sp.spmatrix, config: SolverConfig | None = None,
                 # remaining |C|^2 positions (duplicates merge)
                 fill = min(float(np.sum(offdeg[f].astype(np.float64) ** 2)),
                            float(n_cur - f.size) ** 2)
-                if fill > STALL_FILL_FACTOR * current.nnz and best_f is not None:
-                    break
+                if fill > STALL_FILL_FACTOR * current.nnz:
+                    break  # every cap, the first included, stays under the budget
                 if best_f is None or f.size > best_f.size:
                     best_f = f
             if best_f is not None and best_f.size:
@@ -801,7 +826,8 @@ def _solve_rows(hierarchy: MultigridHierarchy, rows: np.ndarray, config: SolverC
     N.check(N.lib().cf_solve_rows(dev.handle, N.ptr(rows, N.f64p), count,
                                   N.C.byref(_params(config, n)), N.ptr(out, N.f64p),
                                   N.ptr(res, N.f64p), N.C.byref(st)), st)
-    hierarchy.stats.record(res, int(st.fallback_solves), int(st.vcycles))
+    hierarchy.stats.record(res, int(st.fallback_solves), int(st.vcycles),
+                           int(st.krylov_solves))
     return out, res
 
 

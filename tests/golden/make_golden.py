@@ -351,6 +351,21 @@ def config5():
     config_rmat("config5", 22, 12, 5, False, k, q, samp=(1024, 5, 64))
 
 
+def exact10k():
+    """cf_closeness_exact on a 10^4-node BA graph (the reference solves every
+    node, centrality.py:78-101) for the device reduction's parity test."""
+    g = gen.barabasi_albert_graph(10000, 3, 9)
+    query = [0, 17, 4242, 9999]
+    cfg = slv.SolverConfig(tau=1e-8, seed=0)
+    h = slv.setup(cfcent.laplacian(g), cfg)
+    t0 = time.perf_counter()
+    tab = cfcent.cf_closeness_exact(g, h, query, cfg, threads=8)
+    t1 = time.perf_counter()
+    print("exact10k", tab.vector(query), t1 - t0, flush=True)
+    save("exact10k.npz", query=np.array(query), exact=tab.vector(query),
+         sizes=np.array(h.level_sizes), t_exact=np.float64(t1 - t0))
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["kats", "small", "c1", "c2"]
     if "kats" in which:
@@ -363,6 +378,8 @@ if __name__ == "__main__":
         config2()
     if "c3" in which:
         config3()
+    if "exact10k" in which:
+        exact10k()
     if "c4" in which:
         config4()
     if "c5" in which:

@@ -207,3 +207,37 @@ def test_config3_closeness_parity():
             assert err_ours <= max(1e-8, 2 * err_ref), (est, tau, err_ours, err_ref)
             if tau == 1e-10:
                 assert abs(ours[tau][est] / ref - 1) <= 1e-6, (est, tau)
+
+
+def test_exact_closeness_device_reduction_vs_pinv_and_host_route():
+    """cf_closeness_exact reduces the n node solutions on the device
+    (cf_exact_sums); it equals the dense pseudo-inverse value and the host
+    four-term route of resistances_from_node (resistance.py:102-130) summed
+    over every target, at n ~ 1,600 (several 128-column chunks + a tail)."""
+    g = G.barabasi_albert_graph(1600, 3, 11)
+    cfg = P.SolverConfig(tau=1e-10)
+    h = P.setup(P.laplacian(g), cfg)
+    q = [0, 5, 801, 1599]
+    got = P.cf_closeness_exact(g, h, q, cfg).vector(q)
+    r = dense_pinv_resistance(P.laplacian(g).toarray())
+    exact = (g.n - 1) / r[q].sum(axis=1)
+    assert np.allclose(got, exact, rtol=1e-8)
+    cache = {}
+    host = [(g.n - 1) / P.resistances_from_node(h, v, np.arange(g.n), cfg, cache=cache).sum()
+            for v in q]
+    assert np.allclose(got, host, rtol=1e-9)
+    assert h.stats.max_residual <= 1e-10
+
+
+@pytest.mark.slow
+def test_exact_closeness_vs_reference_10k():
+    """n = 10^4 BA graph: device exact closeness vs the reference's own
+    cf_closeness_exact (tests/golden/exact10k.npz, tau 1e-8)."""
+    d = golden("exact10k.npz")
+    g = G.barabasi_albert_graph(10000, 3, 9)
+    cfg = P.SolverConfig(tau=1e-8)
+    h = P.setup(P.laplacian(g), cfg)
+    assert h.level_sizes == d["sizes"].tolist()
+    q = d["query"].tolist()
+    got = P.cf_closeness_exact(g, h, q, cfg).vector(q)
+    assert np.allclose(got, d["exact"], rtol=1e-6), np.abs(got / d["exact"] - 1).max()

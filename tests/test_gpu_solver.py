@@ -291,3 +291,30 @@ def test_krylov_handoff_grid(rng):
         assert np.abs(x[r] - ref).max() <= 1e-7 * np.abs(ref).max()
     assert np.array_equal(P.solve(h, b[7]).values, x[7])
     assert np.array_equal(np.stack([p.values for p in P.solve_many(h, -b[:5])]), -x[:5])
+
+
+def test_pinned_pipeline_error_drains_copies(rng):
+    """an unbalanced column in the SECOND block of the overlapped
+    pinned multi-block path raises DomainError only after the copy stream has
+    drained (no DMA into the caller's buffers after the raise); the next call
+    on the same hierarchy works."""
+    import torch
+    g = G.grid_graph(40)
+    h = P.setup(P.laplacian(g), P.SolverConfig(tau=1e-8))
+    b = rng.standard_normal((200, g.n))
+    b -= b.mean(axis=1, keepdims=True)
+    rows = torch.empty(b.shape, dtype=torch.float64, pin_memory=True).numpy()
+    out = torch.empty(b.shape, dtype=torch.float64, pin_memory=True).numpy()
+    rows[...] = b
+    rows[150, 3] += 1.0  # block 2 (columns 128..199)
+    out[...] = 7.0
+    with pytest.raises(P.DomainError):
+        P.solve_many(h, rows, out=out)
+    snap = out.copy()
+    torch.cuda.synchronize()
+    import time
+    time.sleep(0.05)
+    assert np.array_equal(out, snap)  # nothing still being written
+    rows[150, 3] -= 1.0
+    got = P.solve_many(h, rows, out=out)
+    assert max(p.achieved_residual for p in got) <= 1e-8

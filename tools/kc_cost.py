@@ -48,7 +48,9 @@ for k in (int(x) for x in args.widths.split(",")):
         N.check(N.lib().cf_solve_block_dev(dev.handle, C.c_void_p(b.data_ptr()),
                                            C.c_void_p(x.data_ptr()), k,
                                            C.byref(_params(cfg, n)), N.ptr(res, N.f64p),
-                                           C.byref(st)), st)
+                                           C.byref(st),
+                                           C.c_void_p(torch.cuda.current_stream().cuda_stream)),
+                st)
         torch.cuda.synchronize()
         if r:
             times.append((time.perf_counter() - t0) * 1e3)
