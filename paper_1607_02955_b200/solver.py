@@ -75,7 +75,12 @@ DEVICE_REORDER = os.environ.get("CF_DEVICE_REORDER", "1") != "0"
 # every level when n0 > STALL_BREAKER_MIN_N0; graphs whose hierarchies never
 # stall there (C1-C3) keep the reference hierarchy exactly.
 STALL_ELIM_CAP = 16
-STALL_ELIM_CAPS = (16, 64, 256, 1024)   # escalation, each under the fill budget
+# escalation: the first cap (the reference's kind of low-degree set, one size
+# up) is always a candidate; each larger cap only while its fill bound stays
+# under the budget.  (Applying the budget to the first cap as well drops the
+# elimination candidate on R-MAT hub levels -- the bound sum d_f^2 is a worst
+# case -- and the C5 setup then runs for > 15 min into a many-level hierarchy.)
+STALL_ELIM_CAPS = (16, 64, 256, 1024)
 STALL_FILL_FACTOR = 2.0                 # min(sum d_f^2, |C|^2) <= factor * nnz
 STALL_AGG_CAP = 64
 STALL_AGG_THRESHOLD = 0.0
@@ -750,8 +755,8 @@ def setup(matrix: sp.spmatrix, config: SolverConfig | None = None,
                 # remaining |C|^2 positions (duplicates merge)
                 fill = min(float(np.sum(offdeg[f].astype(np.float64) ** 2)),
                            float(n_cur - f.size) ** 2)
-                if fill > STALL_FILL_FACTOR * current.nnz:
-                    break  # every cap, the first included, stays under the budget
+                if fill > STALL_FILL_FACTOR * current.nnz and best_f is not None:
+                    break  # escalation stops at the first cap over the budget
                 if best_f is None or f.size > best_f.size:
                     best_f = f
             if best_f is not None and best_f.size:
