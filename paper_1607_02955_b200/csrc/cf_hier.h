@@ -23,10 +23,20 @@ struct Plan {
     int64_t* sbeg = nullptr;
     int64_t* send = nullptr;
     std::vector<int64_t> cseg;  // class c -> segments [cseg[c], cseg[c+1])
+    std::vector<int64_t> cheavy;  // class c -> entries in its heavy rows
     int32_t* seg_hv = nullptr;  // segment -> heavy index
     int32_t* h_row = nullptr;   // heavy index -> row
     int32_t* h_pos = nullptr;   // heavy index -> position in class order
     int* cntr = nullptr;        // arrival counters (zero between launches)
+    // Processing order of the segments (scheduling only; partials are still
+    // indexed and summed by segment id): segments sorted by the column window
+    // of their first entry, so the warps in flight gather from one L2-sized
+    // window of X.  sord_cls: sorted inside every sweep launch range (each
+    // Gauss-Seidel class, then the merged Jacobi classes as one range);
+    // sord_all: sorted over the whole plan (k_seg launches).  nullptr: id order.
+    int32_t* sord_cls = nullptr;
+    int32_t* sord_all = nullptr;
+    int64_t nwin_seg = 0;       // segments cut at column-window boundaries
 };
 
 struct DLevel {
@@ -89,6 +99,7 @@ constexpr int kGsClasses = 2;
 // Supported block widths (columns per device chunk).
 constexpr int kMaxKC = 256;
 int pick_kc(int64_t remaining);
+int plan_max_kc(int64_t total);
 
 struct Hier {
     int dev = 0;

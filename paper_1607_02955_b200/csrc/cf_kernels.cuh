@@ -250,6 +250,9 @@ __device__ __forceinline__ void fetch_chunk(const int32_t* __restrict__ col,
 #ifndef CF_GATHER_DOUBLES
 #define CF_GATHER_DOUBLES 16
 #endif
+#ifndef CF_GATHER_ROWS_MAX
+#define CF_GATHER_ROWS_MAX 8
+#endif
 template <int KC, int MODE, int GD = CF_GATHER_DOUBLES>
 __device__ __forceinline__ void gather_row_from(const int32_t* __restrict__ col,
                                                 const double* __restrict__ val, int64_t beg,
@@ -264,7 +267,8 @@ __device__ __forceinline__ void gather_row_from(const int32_t* __restrict__ col,
     constexpr unsigned MASK = W == 32 ? 0xffffffffu : ((1u << W) - 1u);
     // rows in flight per group: GD doubles of row data per lane (default
     // CF_GATHER_DOUBLES, so the gather kernels fit 3 CTAs of 256 threads per SM)
-    constexpr int G0 = GD / V > 0 ? GD / V : 1;
+    // (at most 8 rows: 16 rows of narrow blocks spilled under the register cap)
+    constexpr int G0 = GD / V > 0 ? (GD / V > CF_GATHER_ROWS_MAX ? CF_GATHER_ROWS_MAX : GD / V) : 1;
     constexpr int G = W < G0 ? W : G0;
     int jn = 0;
     double an = 0.0, dn = 1.0;
@@ -399,6 +403,7 @@ struct SegWork {
     const int32_t* h_pos = nullptr;   // heavy index -> position in the class-ordered row list
     int* cntr = nullptr;              // heavy index -> arrivals (kept zero between launches)
     double* SP = nullptr;
+    const int32_t* sord = nullptr;    // launch position -> segment (nullptr: identity)
 };
 
 template <int KC>
@@ -432,6 +437,18 @@ __device__ __forceinline__ bool seg_item(const SegWork& w, int64_t s,
     if (lane == 0) w.cntr[hv] = 0;
     hv_out = hv;
     return true;
+}
+
+// acc += the segment partials of heavy row hv, in segment order
+template <int KC>
+__device__ __forceinline__ void heavy_partials(const HeavyDev& H, int hv, int c0,
+                                               DV<Lay<KC>::VEC>& acc) {
+    constexpr int V = Lay<KC>::VEC;
+    for (int64_t sgi = H.hsp[hv]; sgi < H.hsp[hv + 1]; ++sgi) {
+        DV<V> q = ldv<V>(H.P + (size_t)sgi * KC + c0);
+#pragma unroll
+        for (int t = 0; t < V; ++t) acc.v[t] += q.v[t];
+    }
 }
 
 // Heavy rows use the partials of their segments (k_seg, summed in segment

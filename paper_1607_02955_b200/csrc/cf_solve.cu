@@ -54,14 +54,16 @@ enum ColState { COL_ZERO = 0, COL_ACTIVE = 1, COL_CONV = 2, COL_FALLBACK = 3, CO
 
 // R = B - L X ; partials of sum(R), sum(R^2)  (solver.py:694-695)
 template <int KC>
-__global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : CF_RED_CTAS)) k_residual(int n, const int64_t* __restrict__ rp,
+__global__ void __launch_bounds__(kThreads, (KC > 128 ? 2 : CF_RED_CTAS)) k_residual(int n, const int64_t* __restrict__ rp,
                                                        const int32_t* __restrict__ col,
                                                        const double* __restrict__ val,
                                                        const double* __restrict__ diag,
                                                        const double* __restrict__ B,
                                                        const double* __restrict__ X,
                                                        double* __restrict__ R, RedCtl red,
-                                                       HeavyDev H) {
+                                                       HeavyDev H, int x_zero) {
+    // x_zero: X is known to be all zeros (first check of a solve), so R = B
+    // exactly (b - fma(d, 0, 0) = b) and no matrix entry or row of X is read
     CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
     extern __shared__ double smem[];
@@ -72,11 +74,16 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : CF_RED_CTAS)) k_res
     for (int r = slot; r < kRowsPerPart; r += Lt::RPB) {
         int64_t i = part * kRowsPerPart + r;
         if (i >= n || !lane_ok) break;
-        DV<V> acc;
+        DV<V> acc, x;
         zero(acc);
-        row_sum<KC, G_PLAIN>(H, i, col, val, rp[i], rp[i + 1], nullptr, nullptr, X, c0, acc);
-        DV<V> b = ldv<V>(B + i * KC + c0), x = ldv<V>(X + i * KC + c0);
-        double d = diag[i];
+        zero(x);
+        double d = 0.0;
+        if (!x_zero) {
+            row_sum<KC, G_PLAIN>(H, i, col, val, rp[i], rp[i + 1], nullptr, nullptr, X, c0, acc);
+            x = ldv<V>(X + i * KC + c0);
+            d = diag[i];
+        }
+        DV<V> b = ldv<V>(B + i * KC + c0);
         DV<V> out;
 #pragma unroll
         for (int t = 0; t < V; ++t) {
@@ -92,7 +99,7 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : CF_RED_CTAS)) k_res
 
 // Y = L X (full Laplacian product) -- fallback Krylov solvers (solver.py:571-648)
 template <int KC>
-__global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : CF_RED_CTAS)) k_spmm(int n, const int64_t* __restrict__ rp,
+__global__ void __launch_bounds__(kThreads, (KC > 128 ? 2 : CF_RED_CTAS)) k_spmm(int n, const int64_t* __restrict__ rp,
                                                    const int32_t* __restrict__ col,
                                                    const double* __restrict__ val,
                                                    const double* __restrict__ diag,
@@ -430,7 +437,7 @@ __global__ void __launch_bounds__(kThreads) k_lincomb(int n, double* __restrict_
 // CTAs/SM so the pipeline state does not spill; heavy-row segment CTAs follow
 // the tiles.  Same per-row arithmetic as the warp-per-row form.
 template <int KC, bool SHORT = false>
-__global__ void __launch_bounds__(kThreads, SHORT ? 2 : (KC >= 256 ? 2 : kGatherCtas)) k_gs(const int32_t* __restrict__ rows,
+__global__ void __launch_bounds__(kThreads, SHORT ? 2 : (KC > 128 ? 2 : kGatherCtas)) k_gs(const int32_t* __restrict__ rows,
                                                               int base, int cnt,
                                                               const int64_t* __restrict__ rp,
                                                               const int32_t* __restrict__ col,
@@ -439,7 +446,9 @@ __global__ void __launch_bounds__(kThreads, SHORT ? 2 : (KC >= 256 ? 2 : kGather
                                                               const double* __restrict__ B,
                                                               double* __restrict__ X,
                                                               int from_zero, int jlim, int rpw,
-                                                              HeavyDev H, SegWork w) {
+                                                              HeavyDev H, SegWork w, int pre) {
+    // pre: the heavy rows' segment partials were computed by a preceding k_seg
+    // launch (H.P); otherwise the launch carries the segments itself (w)
     CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
     if (!lane_ok) return;
@@ -469,12 +478,16 @@ __global__ void __launch_bounds__(kThreads, SHORT ? 2 : (KC >= 256 ? 2 : kGather
             row_pipeline<KC, G_PLAIN>(
                 g0 + slot, Lt::RPB, gend, row_of, rp, col, val, nullptr, nullptr,
                 [&](int64_t, int64_t r, int64_t beg, int64_t end, int jj, double aa, double dd) {
-                    if (H.hv && end - beg > kHeavyNnz) return;  // finished by its last segment warp
+                    const bool heavy = H.hv && end - beg > kHeavyNnz;
+                    if (heavy && !pre) return;  // finished by its last segment warp
                     DV<V> b = ldv<V>(B + r * KC + c0);
                     const double d = diag[r];
                     zero(acc);
-                    gather_row_from<KC, G_PLAIN>(col, val, beg, end, nullptr, nullptr, X, c0, acc,
-                                                 jj, aa, dd, jlim);
+                    if (heavy)
+                        heavy_partials<KC>(H, H.hv[r], c0, acc);
+                    else
+                        gather_row_from<KC, G_PLAIN>(col, val, beg, end, nullptr, nullptr, X, c0,
+                                                     acc, jj, aa, dd, jlim);
 #pragma unroll
                     for (int t = 0; t < V; ++t) acc.v[t] = (b.v[t] - acc.v[t]) / d;
                     stv<V>(X + r * KC + c0, acc);
@@ -489,10 +502,14 @@ __global__ void __launch_bounds__(kThreads, SHORT ? 2 : (KC >= 256 ? 2 : kGather
         i = rows ? (int64_t)rows[g] : base + g;
         if (!from_zero) {
             const int64_t beg = rp[i], end = rp[i + 1];
-            if (H.hv && end - beg > kHeavyNnz) return;  // finished by its last segment warp
+            const bool heavy = H.hv && end - beg > kHeavyNnz;
+            if (heavy && !pre) return;  // finished by its last segment warp
             DV<V> b = ldv<V>(B + i * KC + c0);
             const double d = diag[i];
-            gather_row<KC, G_PLAIN>(col, val, beg, end, nullptr, nullptr, X, c0, acc, jlim);
+            if (heavy)
+                heavy_partials<KC>(H, H.hv[i], c0, acc);
+            else
+                gather_row<KC, G_PLAIN>(col, val, beg, end, nullptr, nullptr, X, c0, acc, jlim);
 #pragma unroll
             for (int t = 0; t < V; ++t) acc.v[t] = (b.v[t] - acc.v[t]) / d;
             stv<V>(X + i * KC + c0, acc);
@@ -501,6 +518,7 @@ __global__ void __launch_bounds__(kThreads, SHORT ? 2 : (KC >= 256 ? 2 : kGather
     } else {
         int64_t sg = w.s_lo + (g - cnt);
         if (sg >= w.s_hi) return;
+        if (w.sord) sg = w.sord[sg];
         int hv;
         if (!seg_item<KC>(w, sg, col, val, X, c0, hv, acc, jlim)) return;
         i = w.h_row[hv];
@@ -516,11 +534,11 @@ __global__ void __launch_bounds__(kThreads, SHORT ? 2 : (KC >= 256 ? 2 : kGather
 // for i = rows[q] with every x_j read before any row of the step is written
 // (k_scatter_rows then writes T back).  Heavy rows as in k_gs.
 template <int KC, bool SHORT = false>
-__global__ void __launch_bounds__(kThreads, SHORT ? 2 : (KC >= 256 ? 2 : kGatherCtas)) k_jacobi_rows(
+__global__ void __launch_bounds__(kThreads, SHORT ? 2 : (KC > 128 ? 2 : kGatherCtas)) k_jacobi_rows(
     const int32_t* __restrict__ rows, int base, int cnt, const int64_t* __restrict__ rp,
     const int32_t* __restrict__ col, const double* __restrict__ val,
     const double* __restrict__ diag, const double* __restrict__ B, const double* __restrict__ X,
-    double* __restrict__ T, int jlim, int rpw, HeavyDev H, SegWork w) {
+    double* __restrict__ T, int jlim, int rpw, HeavyDev H, SegWork w, int pre) {
     CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
     if (!lane_ok) return;
@@ -537,12 +555,16 @@ __global__ void __launch_bounds__(kThreads, SHORT ? 2 : (KC >= 256 ? 2 : kGather
             row_pipeline<KC, G_PLAIN>(
                 g0 + slot, Lt::RPB, gend, row_of, rp, col, val, nullptr, nullptr,
                 [&](int64_t qq, int64_t r, int64_t beg, int64_t end, int jj, double aa, double dd) {
-                    if (H.hv && end - beg > kHeavyNnz) return;
+                    const bool heavy = H.hv && end - beg > kHeavyNnz;
+                    if (heavy && !pre) return;
                     DV<V> b = ldv<V>(B + r * KC + c0);
                     const double d = diag[r];
                     zero(acc);
-                    gather_row_from<KC, G_PLAIN>(col, val, beg, end, nullptr, nullptr, X, c0, acc,
-                                                 jj, aa, dd, jlim);
+                    if (heavy)
+                        heavy_partials<KC>(H, H.hv[r], c0, acc);
+                    else
+                        gather_row_from<KC, G_PLAIN>(col, val, beg, end, nullptr, nullptr, X, c0,
+                                                     acc, jj, aa, dd, jlim);
 #pragma unroll
                     for (int t = 0; t < V; ++t) acc.v[t] = (b.v[t] - acc.v[t]) / d;
                     stv<V>(T + qq * KC + c0, acc);
@@ -557,10 +579,14 @@ __global__ void __launch_bounds__(kThreads, SHORT ? 2 : (KC >= 256 ? 2 : kGather
         i = rows ? (int64_t)rows[g] : base + g;
         q = g;
         const int64_t beg = rp[i], end = rp[i + 1];
-        if (H.hv && end - beg > kHeavyNnz) return;
+        const bool heavy = H.hv && end - beg > kHeavyNnz;
+        if (heavy && !pre) return;
         DV<V> b = ldv<V>(B + i * KC + c0);
         const double d = diag[i];
-        gather_row<KC, G_PLAIN>(col, val, beg, end, nullptr, nullptr, X, c0, acc, jlim);
+        if (heavy)
+            heavy_partials<KC>(H, H.hv[i], c0, acc);
+        else
+            gather_row<KC, G_PLAIN>(col, val, beg, end, nullptr, nullptr, X, c0, acc, jlim);
 #pragma unroll
         for (int t = 0; t < V; ++t) acc.v[t] = (b.v[t] - acc.v[t]) / d;
         stv<V>(T + q * KC + c0, acc);
@@ -568,6 +594,7 @@ __global__ void __launch_bounds__(kThreads, SHORT ? 2 : (KC >= 256 ? 2 : kGather
     }
     int64_t sg = w.s_lo + (g - cnt);
     if (sg >= w.s_hi) return;
+    if (w.sord) sg = w.sord[sg];
     int hv;
     if (!seg_item<KC>(w, sg, col, val, X, c0, hv, acc, jlim)) return;
     i = w.h_row[hv];
@@ -600,7 +627,7 @@ __global__ void __launch_bounds__(kThreads) k_scatter_rows(const int32_t* __rest
 // them in piece order (fixed order, independent of scheduling).
 constexpr int kAggPiece = 8;
 template <int KC>
-__global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : CF_RED_CTAS)) k_agg_restrict(
+__global__ void __launch_bounds__(kThreads, (KC > 128 ? 2 : CF_RED_CTAS)) k_agg_restrict(
     int64_t np, const int32_t* __restrict__ pa, const int32_t* __restrict__ pb,
     const int32_t* __restrict__ pslot, int* __restrict__ acnt, double* __restrict__ PP,
     const int32_t* __restrict__ aptr, const int32_t* __restrict__ amem,
@@ -657,8 +684,10 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : CF_RED_CTAS)) k_agg
 
 // Line-search partials (solver.py:550-556): den = d . L d with d = P xc over
 // fine rows (CTAs [0, pf)), num = r . d = bc . xc over coarse rows (CTAs [pf, pf+pc)).
+// agg == nullptr: the rows are the coarse level's own (den = xc . L_c xc with
+// the Galerkin operator L_c = P^T L P, the same quantity over fewer nonzeros).
 template <int KC>
-__global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : CF_RED_CTAS)) k_agg_ls(
+__global__ void __launch_bounds__(kThreads, (KC > 128 ? 2 : CF_RED_CTAS)) k_agg_ls(
     int n, int nc, const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
     const double* __restrict__ val, const double* __restrict__ diag,
     const int32_t* __restrict__ agg, const double* __restrict__ Xc,
@@ -677,7 +706,7 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : CF_RED_CTAS)) k_agg
             DV<V> acc;
             zero(acc);
             row_sum<KC, G_PLAIN>(H, i, col, val, rp[i], rp[i + 1], nullptr, nullptr, Xc, c0, acc);
-            DV<V> d = ldv<V>(Xc + (size_t)agg[i] * KC + c0);
+            DV<V> d = ldv<V>(Xc + (size_t)(agg ? agg[i] : i) * KC + c0);
             double dg = diag[i];
 #pragma unroll
             for (int t = 0; t < V; ++t) {
@@ -722,7 +751,7 @@ __global__ void __launch_bounds__(kThreads) k_agg_correct(int n, const int32_t* 
 
 // bc_i = b[c_i] + sum_f W_cf(i,f) * (b_f / d_f)  (solver.py:534-536)
 template <int KC>
-__global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : CF_RED_CTAS)) k_elim_restrict(
+__global__ void __launch_bounds__(kThreads, (KC > 128 ? 2 : CF_RED_CTAS)) k_elim_restrict(
     int nc, const int32_t* __restrict__ cn, const int64_t* __restrict__ wp,
     const int32_t* __restrict__ wc, const double* __restrict__ wv,
     const int32_t* __restrict__ fn, const double* __restrict__ fd,
@@ -744,7 +773,7 @@ __global__ void __launch_bounds__(kThreads, (KC >= 256 ? 2 : CF_RED_CTAS)) k_eli
 // DEEP: launches with few segments (a handful per SM) are latency-bound, so
 // every warp keeps 4x the neighbour rows in flight (1 CTA/SM by registers).
 template <int KC, int MODE, bool DEEP = false>
-__global__ void __launch_bounds__(kThreads, DEEP ? 1 : (KC >= 256 ? 2 : kGatherCtas)) k_seg(int64_t s_lo, int64_t s_hi,
+__global__ void __launch_bounds__(kThreads, DEEP ? 1 : (KC > 128 ? 2 : kGatherCtas)) k_seg(int64_t s_lo, int64_t s_hi,
                                                   const int64_t* __restrict__ sbeg,
                                                   const int64_t* __restrict__ send,
                                                   const int32_t* __restrict__ col,
@@ -752,15 +781,17 @@ __global__ void __launch_bounds__(kThreads, DEEP ? 1 : (KC >= 256 ? 2 : kGatherC
                                                   const int32_t* __restrict__ map,
                                                   const double* __restrict__ div,
                                                   const double* __restrict__ X,
-                                                  double* __restrict__ P) {
+                                                  double* __restrict__ P,
+                                                  const int32_t* __restrict__ sord, int jlim) {
     CF_PDL_ENTRY();
     CF_LANE_SETUP(KC)
     int64_t sg = s_lo + (int64_t)blockIdx.x * Lt::RPB + slot;
     if (sg >= s_hi || !lane_ok) return;
+    if (sord) sg = sord[sg];
     DV<V> acc;
     zero(acc);
     gather_row<KC, MODE, DEEP ? 4 * CF_GATHER_DOUBLES : CF_GATHER_DOUBLES>(
-        col, val, sbeg[sg], send[sg], map, div, X, c0, acc);
+        col, val, sbeg[sg], send[sg], map, div, X, c0, acc, jlim);
     stv<V>(P + (size_t)sg * KC + c0, acc);
 }
 
@@ -846,7 +877,11 @@ __global__ void __launch_bounds__(kThreads) k_dense_small(int n, int chunk,
 #endif
 constexpr int kGR = 128, kGL = 16, kDenseTC = CF_DENSE_TC;
 template <int KC>
-constexpr int dense_tc() { return KC < kDenseTC ? KC : kDenseTC; }
+constexpr int dense_tc() {
+    // column tile: the widest of kDenseTC / 64 / 32 that divides the block
+    // (160 -> 32, 192 -> 64); the sum order per output does not depend on it
+    return KC < kDenseTC ? KC : KC % kDenseTC == 0 ? kDenseTC : KC % 64 == 0 ? 64 : 32;
+}
 template <int KC>
 __global__ void __launch_bounds__(kThreads) k_dense_tile(int n, int chunk,
                                                          const double* __restrict__ M,
@@ -1085,6 +1120,7 @@ struct Ops {
     static SegWork segwork(const Hier& h, const Plan& pl, int64_t lo, int64_t hi) {
         SegWork w;
         if (!pl.nheavy || hi <= lo) return w;
+        w.sord = pl.sord_cls;
         w.s_lo = lo;
         w.s_hi = hi;
         w.sbeg = pl.sbeg;
@@ -1098,31 +1134,57 @@ struct Ops {
         return w;
     }
     // segment partials of a plan's segments [lo, hi)
+    // sweep = true: [lo, hi) is a sweep launch range (a Gauss-Seidel class or
+    // the merged Jacobi classes; window order sord_cls), hnnz its entry count
+    // (-1: the whole plan, window order sord_all)
     template <int MODE>
     static void seg(Hier& h, const Plan& pl, int64_t lo, int64_t hi, const int32_t* col,
                     const double* val, const int32_t* map, const double* div, const double* X,
-                    int level) {
+                    int level, bool sweep = false, double hnnz = -1.0, int jlim = 0x7fffffff) {
         if (hi <= lo) return;
-        const double hnnz = (lo == 0 && hi == pl.nseg) ? (double)pl.heavy_nnz
-                                                       : (double)kSegNnz * (hi - lo);
+        if (hnnz < 0)
+            hnnz = (lo == 0 && hi == pl.nseg) ? (double)pl.heavy_nnz : (double)kSegNnz * (hi - lo);
         ProfScope ps(h, "heavy_seg", level, 12.0 * hnnz + Vb(hi - lo) * 2, Vb(hnnz));
         const unsigned grid = (unsigned)((hi - lo + Lay<KC>::RPB - 1) / Lay<KC>::RPB);
+        const int32_t* ord = sweep ? pl.sord_cls
+                                   : (lo == 0 && hi == pl.nseg) ? pl.sord_all : nullptr;
         if (grid <= kDeepSegCtas)
             launch_k(k_seg<KC, MODE, true>, dim3(grid), dim3(kThreads), 0, h.s, lo, hi, pl.sbeg,
-                     pl.send, col, val, map, div, X, h.SP);
+                     pl.send, col, val, map, div, X, h.SP, ord, jlim);
         else
             launch_k(k_seg<KC, MODE, false>, dim3(grid), dim3(kThreads), 0, h.s, lo, hi, pl.sbeg,
-                     pl.send, col, val, map, div, X, h.SP);
+                     pl.send, col, val, map, div, X, h.SP, ord, jlim);
     }
-    static void residual(Hier& h, const double* B, const double* X, double* R, double* sums2) {
+    // Sweeps over a launch range with at least this many heavy-row segments
+    // compute the partials in a k_seg launch of their own (no fence / arrival
+    // counter per segment: the same L1 matrix gathers at 10.9 TB/s in k_seg and
+    // 6.3 TB/s inside the sweep kernel, profiles/r02); smaller ranges keep the
+    // segments inside the sweep launch (one launch less on small levels).
+    // Either way a heavy row is the sum of its partials in segment order.
+    static int64_t pre_seg_min() {
+        static const int64_t v = [] {
+            const char* e = std::getenv("CF_PRE_SEG_MIN");
+            return e ? (int64_t)std::atoll(e) : (int64_t)8192;
+        }();
+        return v;
+    }
+    static void residual(Hier& h, const double* B, const double* X, double* R, double* sums2,
+                         bool x_zero = false) {
         DLevel& l = h.L[0];
         int64_t np = nparts_of(l.n);
+        if (x_zero) {
+            ProfScope ps(h, "residual0", 0, Vb(l.n) * (R ? 2 : 1));
+            launch_k(k_residual<KC>, dim3((unsigned)np), dim3(kThreads), red_smem<KC, 2>(), h.s,
+                     l.n, l.rp, l.col, l.val, l.diag, B, X, R, redctl(h, h.parts, np, sums2, 0),
+                     HeavyDev{}, 1);
+            return;
+        }
         seg<G_PLAIN>(h, l.pm, 0, l.pm.nseg, l.col, l.val, nullptr, nullptr, X, 0);
         const int64_t light = l.nnz - l.pm.heavy_nnz;  // heavy rows: the k_seg launch above
         ProfScope ps(h, "residual", 0, A(l.n, light) + Vb(l.n) * (R ? 3 : 2), Vb(light));
         launch_k(k_residual<KC>, dim3((unsigned)np), dim3(kThreads), red_smem<KC, 2>(), h.s, l.n,
                  l.rp, l.col, l.val, l.diag, B, X, R, redctl(h, h.parts, np, sums2, 0),
-                 hd(h, l.pm));
+                 hd(h, l.pm), 0);
     }
     static void colsum(Hier& h, const double* X, const double* Y, double* out) {
         int n = h.n0;
@@ -1158,6 +1220,13 @@ struct Ops {
     static void zero_block(Hier& h, double* x, int64_t elems) {
         launch_k(k_zero_block<KC>, dim3((unsigned)((elems + kThreads - 1) / kThreads)), dim3(kThreads), 0, h.s, elems,
                                                                                           x);
+    }
+    static bool coarse_ls() {
+        static const bool on = [] {
+            const char* e = std::getenv("CF_COARSE_LS");
+            return !e || std::atoi(e) != 0;
+        }();
+        return on;
     }
     static double* bufb(Hier& h, int j) { return j == 0 ? h.R : h.L[j].b; }
     static double* bufx(Hier& h, int j) { return j == 0 ? h.C : h.L[j].x; }
@@ -1233,7 +1302,18 @@ struct Ops {
         }
         cycle(h, j + 1, nu1, nu2);
         int64_t pf = nparts_of(l.n), pc = nparts_of(l.nc);
-        {
+        if (coarse_ls() && c.kind == CF_LEVEL_AGGREGATION && c.rp) {
+            // d . L d = xc . (P^T L P) xc: the coarse level's Galerkin operator
+            // gives the same denominator from nnz(L_c) instead of nnz(L) gathers
+            pf = nparts_of(c.n);
+            seg<G_PLAIN>(h, c.pm, 0, c.pm.nseg, c.col, c.val, nullptr, nullptr, xc, j + 1);
+            const int64_t light = c.nnz - c.pm.heavy_nnz;
+            ProfScope ps(h, "agg_linesearch", j, A(c.n, light) + Vb(2 * l.nc), Vb(light));
+            launch_k(k_agg_ls<KC>, dim3((unsigned)(pf + pc)), dim3(kThreads), red_smem<KC, 1>(),
+                     h.s, c.n, l.nc, c.rp, c.col, c.val, c.diag, (const int32_t*)nullptr, xc, bc,
+                     redctl(h, h.parts, pf, l.ls, 0), redctl(h, h.parts + pf * KC, pc, l.ls + KC, 1),
+                     hd(h, c.pm));
+        } else {
             seg<G_PLAIN>(h, l.pm, 0, l.pm.nseg, l.cagg, l.val, nullptr, nullptr, xc, j);
             const int64_t light = l.nnz - l.pm.heavy_nnz;
             ProfScope ps(h, "agg_linesearch", j, A(l.n, light) + 4.0 * l.n + Vb(2 * l.nc),
@@ -1259,24 +1339,28 @@ struct Ops {
         int beg = l.cptr[colr], cnt = l.cptr[colr + 1] - beg;
         if (cnt <= 0) return;
         const int lev = (int)(&l - &h.L[0]);
-        SegWork w = segwork(h, l.pm, from_zero ? 0 : l.pm.cseg[colr],
-                            from_zero ? 0 : l.pm.cseg[colr + 1]);
-        const int64_t gnnz = from_zero ? 0 : first ? l.c_nnz_lo[colr] : l.c_nnz[colr];
+        const int64_t s_lo = from_zero ? 0 : l.pm.cseg[colr], s_hi = from_zero ? 0 : l.pm.cseg[colr + 1];
+        const int jlim = first ? beg : 0x7fffffff;
+        const int pre = (l.pm.nheavy && s_hi - s_lo >= pre_seg_min()) ? 1 : 0;
+        if (pre)
+            seg<G_PLAIN>(h, l.pm, s_lo, s_hi, l.col, l.val, nullptr, nullptr, x, lev, true,
+                         (double)l.pm.cheavy[colr], jlim);
+        SegWork w = pre ? SegWork{} : segwork(h, l.pm, s_lo, s_hi);
+        const int64_t hvy = pre ? l.pm.cheavy[colr] : 0;  // entries gathered by the k_seg launch
+        const int64_t gnnz = from_zero ? 0 : first ? l.c_nnz_lo[colr] : l.c_nnz[colr] - hvy;
         const int64_t gnbr = from_zero ? 0 : first ? l.c_nbr_lo[colr] : l.c_nbr[colr];
-        ProfScope ps(h, "gs_sweep", lev, 12.0 * l.c_nnz[colr] + 20.0 * cnt + Vb(2 * cnt + gnbr),
-                     Vb(gnnz));
+        ProfScope ps(h, "gs_sweep", lev,
+                     12.0 * (l.c_nnz[colr] - hvy) + 20.0 * cnt + Vb(2 * cnt + gnbr), Vb(gnnz));
         const int rpw = short_rpw(cnt, l.c_nnz[colr]);
         if (rpw > 1)
             launch_k(k_gs<KC, true>,
                      dim3(grid_tiles(cnt, 1, rpw) + grid_rows<KC>(w.s_hi - w.s_lo, 0)),
                      dim3(kThreads), 0, h.s, l.contig ? nullptr : l.crows + beg, beg, cnt, l.rp,
-                     l.col, l.val, l.diag, b, x, from_zero ? 1 : 0, first ? beg : 0x7fffffff,
-                     rpw, hd(h, l.pm), w);
+                     l.col, l.val, l.diag, b, x, from_zero ? 1 : 0, jlim, rpw, hd(h, l.pm), w, pre);
         else
             launch_k(k_gs<KC, false>, dim3(grid_rows<KC>(cnt + (w.s_hi - w.s_lo))),
                      dim3(kThreads), 0, h.s, l.contig ? nullptr : l.crows + beg, beg, cnt, l.rp,
-                     l.col, l.val, l.diag, b, x, from_zero ? 1 : 0, first ? beg : 0x7fffffff, 1,
-                     hd(h, l.pm), w);
+                     l.col, l.val, l.diag, b, x, from_zero ? 1 : 0, jlim, 1, hd(h, l.pm), w, pre);
     }
 
     static void jacobi(Hier& h, DLevel& l, const double* b, double* x, bool first) {
@@ -1284,26 +1368,33 @@ struct Ops {
         int beg = l.cptr[K], cnt = l.cptr[l.ncolors] - beg;
         if (cnt <= 0) return;
         const int lev = (int)(&l - &h.L[0]);
-        SegWork w = segwork(h, l.pm, l.pm.cseg[K], l.pm.cseg[l.ncolors]);
-        int64_t nnz = 0;
-        for (int c = K; c < l.ncolors; ++c) nnz += l.c_nnz[c];
-        const int64_t gnnz = first ? l.merged_nnz_lo : nnz;
+        const int64_t s_lo = l.pm.cseg[K], s_hi = l.pm.cseg[l.ncolors];
+        const int jlim = first ? beg : 0x7fffffff;
+        const int pre = (l.pm.nheavy && s_hi - s_lo >= pre_seg_min()) ? 1 : 0;
+        int64_t nnz = 0, hvy = 0;
+        for (int c = K; c < l.ncolors; ++c) {
+            nnz += l.c_nnz[c];
+            if (pre) hvy += l.pm.cheavy[c];
+        }
+        if (pre)
+            seg<G_PLAIN>(h, l.pm, s_lo, s_hi, l.col, l.val, nullptr, nullptr, x, lev, true,
+                         (double)hvy, jlim);
+        SegWork w = pre ? SegWork{} : segwork(h, l.pm, s_lo, s_hi);
+        const int64_t gnnz = first ? l.merged_nnz_lo : nnz - hvy;
         const int64_t gnbr = first ? l.merged_nbr_lo : l.merged_nbr;
         {
-            ProfScope ps(h, "jacobi_merged", lev, 12.0 * nnz + 20.0 * cnt + Vb(2 * cnt + gnbr),
-                         Vb(gnnz));
+            ProfScope ps(h, "jacobi_merged", lev,
+                         12.0 * (nnz - hvy) + 20.0 * cnt + Vb(2 * cnt + gnbr), Vb(gnnz));
             const int rpw = short_rpw(cnt, nnz);
             if (rpw > 1)
                 launch_k(k_jacobi_rows<KC, true>,
                          dim3(grid_tiles(cnt, 1, rpw) + grid_rows<KC>(w.s_hi - w.s_lo, 0)),
                          dim3(kThreads), 0, h.s, l.contig ? nullptr : l.crows + beg, beg, cnt,
-                         l.rp, l.col, l.val, l.diag, b, x, h.T, first ? beg : 0x7fffffff, rpw,
-                         hd(h, l.pm), w);
+                         l.rp, l.col, l.val, l.diag, b, x, h.T, jlim, rpw, hd(h, l.pm), w, pre);
             else
                 launch_k(k_jacobi_rows<KC, false>, dim3(grid_rows<KC>(cnt + (w.s_hi - w.s_lo))),
                          dim3(kThreads), 0, h.s, l.contig ? nullptr : l.crows + beg, beg, cnt,
-                         l.rp, l.col, l.val, l.diag, b, x, h.T, first ? beg : 0x7fffffff, 1,
-                         hd(h, l.pm), w);
+                         l.rp, l.col, l.val, l.diag, b, x, h.T, jlim, 1, hd(h, l.pm), w, pre);
         }
         ProfScope ps(h, "jacobi_scatter", lev, Vb(2 * cnt) + 4.0 * cnt);
         launch_k(k_scatter_rows<KC>, dim3(grid_rows<KC>(cnt)), dim3(kThreads), 0, h.s, 
@@ -1795,7 +1886,7 @@ static void solve_block_t(Hier& h, int ncols, const CfSolveParams& p, double* re
         CF_CUDA(cudaMemsetAsync(h.d_iter, 0, sizeof(int), h.s));
         CF_CUDA(cudaMemsetAsync(h.d_vcyc, 0, sizeof(long long), h.s));
         CF_CUDA(cudaMemsetAsync(h.d_ncyc, 0, sizeof(int), h.s));
-        O::residual(h, h.B, h.X, h.R, h.sums);
+        O::residual(h, h.B, h.X, h.R, h.sums, /*x_zero=*/true);
         O::status(h, p, cudaGraphConditionalHandle{}, 0);
         CF_CUDA(cudaMemcpyAsync(h.h_count, h.count, sizeof(int), cudaMemcpyDeviceToHost, h.s));
         CF_CUDA(cudaStreamSynchronize(h.s));
@@ -1913,6 +2004,15 @@ static void solve_block_t(Hier& h, int ncols, const CfSolveParams& p, double* re
 // and widths 16..64 cost about the same as each other, so full chunks are 128
 // wide and a tail takes the smallest width that holds it.
 int pick_kc(int64_t rem) {
+    // A remainder of 129..192 columns runs as ONE chunk of width 160 / 192
+    // (5 / 6 columns per lane) instead of a full chunk plus a narrow tail: a
+    // narrow chunk costs ~60 % of a full one (the per-nonzero index and
+    // latency cost does not shrink with the width), a 25-50 % wider one
+    // 25-50 % more.  CF_WIDE_TAIL=0 restores full chunk + tail.
+    static const bool wide_tail = [] {
+        const char* e = std::getenv("CF_WIDE_TAIL");
+        return !e || std::atoi(e) != 0;
+    }();
     static const int sizes[] = {1, 8, 16, 32, 64, 128, 256};
     static const int cap = [] {
         const char* e = std::getenv("CF_MAX_KC");
@@ -1922,14 +2022,27 @@ int pick_kc(int64_t rem) {
             if (s <= c) best = s;
         return best;
     }();
+    if (wide_tail && cap == 128 && rem > 128 && rem <= 192) return rem <= 160 ? 160 : 192;
     if (rem >= cap) return cap;
     for (int s : sizes)
         if (s >= rem) return s;
     return cap;
 }
 
+// widest chunk of the plan pick_kc makes for `total` columns (the workspace is
+// sized once, before the first chunk, so it never regrows between chunks)
+int plan_max_kc(int64_t total) {
+    int kmax = 1;
+    for (int64_t o = 0; o < total;) {
+        const int kc = pick_kc(total - o);
+        kmax = std::max(kmax, kc);
+        o += std::min<int64_t>(kc, total - o);
+    }
+    return kmax;
+}
+
 static int kc_at_least(int k) {
-    static const int sizes[] = {1, 8, 16, 32, 64, 128, 256};
+    static const int sizes[] = {1, 8, 16, 32, 64, 128, 160, 192, 256};
     for (int s : sizes)
         if (s >= k) return s;
     return 256;
@@ -1943,6 +2056,8 @@ static int kc_at_least(int k) {
         case 32: { constexpr int K_ = 32; __VA_ARGS__; } break;   \
         case 64: { constexpr int K_ = 64; __VA_ARGS__; } break;   \
         case 128: { constexpr int K_ = 128; __VA_ARGS__; } break; \
+        case 160: { constexpr int K_ = 160; __VA_ARGS__; } break; \
+        case 192: { constexpr int K_ = 192; __VA_ARGS__; } break; \
         case 256: { constexpr int K_ = 256; __VA_ARGS__; } break; \
         default: throw CfError(CF_RUNTIME, "unsupported block width"); \
     }
@@ -2242,16 +2357,43 @@ extern "C" int cf_device_count(void) {
 template <typename T>
 static T* upload(Hier& h, const T* src, size_t cnt);
 
+// Column windows.  On a level whose X block is far
+// larger than the L2, rows with at least win_deg() entries are cut into
+// segments at multiples of win_rows() columns as well as every kSegNnz
+// entries, and all segments of a launch are processed window by window: the
+// warps in flight then gather from one window of X (win_rows x 8 KC bytes,
+// 32 MB at KC = 128) that stays in the L2 while every hub row consumes it.
+static int64_t win_rows() {
+    static const int64_t w = [] {
+        const char* e = std::getenv("CF_WIN_ROWS");
+        return e ? (int64_t)std::atoll(e) : (int64_t)32768;
+    }();
+    return w;
+}
+static int64_t win_deg() {
+    static const int64_t d = [] {
+        const char* e = std::getenv("CF_WIN_DEG");
+        return e ? (int64_t)std::atoll(e) : (int64_t)256;
+    }();
+    return d;
+}
+
 // Build the heavy-row plan of a CSR operator: rows visited in class order
-// (order == nullptr: natural order, one class).
+// (order == nullptr: natural order, one class).  col != nullptr (sorted rows)
+// enables the column windows; merged_from = first class of the merged Jacobi
+// range (the sweep launch ranges are the classes below it and the merged rest).
 static Plan build_plan(Hier& h, int64_t n, const int64_t* rp, const int32_t* order,
-                       const int32_t* cls_ptr, int ncls) {
+                       const int32_t* cls_ptr, int ncls, const int32_t* col = nullptr,
+                       int merged_from = 0x7fffffff) {
     Plan pl;
     std::vector<int32_t> hv(n, -1), shv, hrow, hpos;
     std::vector<int64_t> hsp{0}, sb, se;
     if (!order) ncls = 1;
+    const int64_t W = win_rows();
+    const bool windows = col && W > 0 && n >= 4 * W;
     for (int c = 0; c < ncls; ++c) {
         pl.cseg.push_back((int64_t)sb.size());
+        pl.cheavy.push_back(0);
         int64_t lo = order ? cls_ptr[c] : 0, hi = order ? cls_ptr[c + 1] : n;
         for (int64_t q = lo; q < hi; ++q) {
             int64_t i = order ? order[q] : q;
@@ -2261,10 +2403,25 @@ static Plan build_plan(Hier& h, int64_t n, const int64_t* rp, const int32_t* ord
             hrow.push_back((int32_t)i);
             hpos.push_back((int32_t)q);
             pl.heavy_nnz += deg;
-            for (int64_t b = rp[i]; b < rp[i + 1]; b += kSegNnz) {
-                sb.push_back(b);
-                se.push_back(std::min<int64_t>(b + kSegNnz, rp[i + 1]));
-                shv.push_back((int32_t)pl.nheavy);
+            pl.cheavy.back() += deg;
+            if (windows && deg >= win_deg()) {
+                int64_t b = rp[i];
+                while (b < rp[i + 1]) {
+                    const int64_t wnd = col[b] / W;
+                    int64_t e = b + 1;
+                    while (e < rp[i + 1] && e - b < kSegNnz && col[e] / W == wnd) ++e;
+                    sb.push_back(b);
+                    se.push_back(e);
+                    shv.push_back((int32_t)pl.nheavy);
+                    ++pl.nwin_seg;
+                    b = e;
+                }
+            } else {
+                for (int64_t b = rp[i]; b < rp[i + 1]; b += kSegNnz) {
+                    sb.push_back(b);
+                    se.push_back(std::min<int64_t>(b + kSegNnz, rp[i + 1]));
+                    shv.push_back((int32_t)pl.nheavy);
+                }
             }
             pl.nheavy++;
             hsp.push_back((int64_t)sb.size());
@@ -2282,6 +2439,22 @@ static Plan build_plan(Hier& h, int64_t n, const int64_t* rp, const int32_t* ord
         pl.h_pos = upload(h, hpos.data(), hpos.size());
         pl.cntr = (int*)h.dalloc(sizeof(int) * pl.nheavy);
         CF_CUDA(cudaMemset(pl.cntr, 0, sizeof(int) * pl.nheavy));
+        if (windows) {
+            // processing orders: stable sort by the window of the first entry
+            std::vector<int32_t> key((size_t)pl.nseg), ord((size_t)pl.nseg);
+            for (int64_t sgi = 0; sgi < pl.nseg; ++sgi) key[(size_t)sgi] = (int32_t)(col[sb[(size_t)sgi]] / W);
+            auto sort_range = [&](int64_t a, int64_t b) {
+                for (int64_t t = a; t < b; ++t) ord[(size_t)t] = (int32_t)t;
+                std::stable_sort(ord.begin() + a, ord.begin() + b,
+                                 [&](int32_t x, int32_t y) { return key[(size_t)x] < key[(size_t)y]; });
+            };
+            const int K = std::min(ncls, std::max(0, merged_from));
+            for (int c = 0; c < K; ++c) sort_range(pl.cseg[c], pl.cseg[c + 1]);
+            sort_range(pl.cseg[K], pl.nseg);
+            pl.sord_cls = upload(h, ord.data(), ord.size());
+            sort_range(0, pl.nseg);
+            pl.sord_all = upload(h, ord.data(), ord.size());
+        }
     }
     h.max_nseg = std::max(h.max_nseg, pl.nseg);
     return pl;
@@ -2293,6 +2466,20 @@ static T* upload(Hier& h, const T* src, size_t cnt) {
     T* d = (T*)h.dalloc(sizeof(T) * cnt);
     CF_CUDA(cudaMemcpy(d, src, sizeof(T) * cnt, cudaMemcpyHostToDevice));
     return d;
+}
+
+// Gauss-Seidel classes of a level with n rows (experiment knobs CF_GS_CLASSES,
+// CF_GS_SMALL_ROWS)
+static int gs_classes_for(int n) {
+    static const int gs_env = [] {
+        const char* e = std::getenv("CF_GS_CLASSES");
+        return e ? std::max(0, std::atoi(e)) : kGsClasses;
+    }();
+    static const int gs_small = [] {  // levels below this many rows
+        const char* e = std::getenv("CF_GS_SMALL_ROWS");
+        return e ? std::atoi(e) : 0;
+    }();
+    return n < gs_small ? 0 : gs_env;
 }
 
 extern "C" int cf_hier_create(int32_t nlev, const CfLevelDesc* ds, int32_t device,
@@ -2322,23 +2509,16 @@ extern "C" int cf_hier_create(int32_t nlev, const CfLevelDesc* ds, int32_t devic
                 if (!l.val) l.val = (double*)h->dalloc(8);
                 l.diag = upload(*h, d.diag, (size_t)d.n);
                 if (d.kind == CF_LEVEL_AGGREGATION)
-                    l.pm = build_plan(*h, d.n, d.rowptr, d.color_rows, d.color_ptr, d.n_colors);
+                    l.pm = build_plan(*h, d.n, d.rowptr, d.color_rows, d.color_ptr, d.n_colors,
+                                      d.col, std::min(d.n_colors, gs_classes_for(d.n)));
                 else
-                    l.pm = build_plan(*h, d.n, d.rowptr, nullptr, nullptr, 1);
+                    l.pm = build_plan(*h, d.n, d.rowptr, nullptr, nullptr, 1, d.col);
             } else if (need_matrix) {
                 throw CfError(CF_DOMAIN, "level matrix missing");
             }
             if (d.kind == CF_LEVEL_AGGREGATION) {
                 l.ncolors = d.n_colors;
-                static const int gs_env = [] {
-                    const char* e = std::getenv("CF_GS_CLASSES");
-                    return e ? std::max(0, std::atoi(e)) : kGsClasses;
-                }();
-                static const int gs_small = [] {  // levels below this many rows
-                    const char* e = std::getenv("CF_GS_SMALL_ROWS");
-                    return e ? std::atoi(e) : 0;
-                }();
-                const int gsk = d.n < gs_small ? 0 : gs_env;
+                const int gsk = gs_classes_for(d.n);
                 l.gs_classes = std::min(d.n_colors, gsk);
                 l.merged = d.n_colors > gsk;
                 if (l.merged)
@@ -2575,10 +2755,10 @@ extern "C" int cf_solve_rows(void* hp, const double* rows, int64_t count,
         CF_CUDA(cudaStreamSynchronize(h.cs));
         done = count;
     }
+    if (done < count) h.ensure_workspace(plan_max_kc(count - done));
     while (done < count) {
         int kc = pick_kc(count - done);
         int cnt = (int)std::min<int64_t>(kc, count - done);
-        h.ensure_workspace(kc);
         h2d_staged(h, h.S, rows + done * n, sizeof(double) * cnt * n);
         rows_to_block(h, h.S, cnt, kc, h.B);
         std::vector<double> res(kc, 0.0);

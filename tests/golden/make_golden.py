@@ -309,7 +309,7 @@ def config_rmat(name, scale, ef, seed, weighted, k, query_fn, jl_rows=32, samp=N
     cfg0 = slv.SolverConfig(tau=tau_list[0], seed=0)
     # the reference setup takes tens of minutes to hours here: keep a pickled
     # copy (scratch, outside the repo) so an interrupted run resumes at the solves
-    cache = os.path.join("/tmp", "golden_cache", f"{name}_hier.pkl")
+    cache = os.path.join(os.path.dirname(OUT), "..", "gpurun_out", "cache", f"{name}_hier.pkl")
     if os.path.exists(cache) and "t_setup" in d:
         import pickle
         with open(cache, "rb") as f:
