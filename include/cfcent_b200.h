@@ -223,6 +223,33 @@ int cf_rebuild_laplacian(int64_t n, const int64_t* indptr, const int64_t* indice
  * indptr: n+1; indices/weights: room for 2m entries; *nnz = entries written. */
 int cf_build_csr(int64_t n, int64_t m, const int64_t* u, const int64_t* v, const double* w,
                  int64_t* indptr, int64_t* indices, double* weights, int64_t* nnz);
+/* Device-side ingestion (csrc/cf_graph.cu).
+ * cf_csr_from_edges_dev: the cf_build_csr contract computed on GPU `device`
+ * (stable radix sort of the 2m adjacency entries by (row, col)); host arrays
+ * in and out.  *status: 0 = written; 1 = duplicate edges present, nothing
+ * written (the caller sums them on the host in the reference's order);
+ * 2 = an edge is a self-loop or out of range.
+ * cf_components_dev: root[i] = smallest node id of i's connected component
+ * (graph.py:217-250 derives the largest component from these labels);
+ * *rounds = hook/jump rounds used. */
+int cf_csr_from_edges_dev(int32_t device, int64_t n, int64_t m, const int64_t* u,
+                          const int64_t* v, const double* w, int64_t* indptr, int64_t* indices,
+                          double* weights, int32_t* status);
+int cf_components_dev(int32_t device, int64_t n, int64_t m, const int64_t* eu, const int64_t* ev,
+                      int64_t* root, int32_t* rounds);
+/* Device-side coarse operators of the setup (
+ * csrc/cf_setup_dev.cu).  L: n x n CSR with stored diagonal and sorted rows;
+ * map[i] = coarse index of node i.  nf = 0: Galerkin product P^T L P of the
+ * aggregation `map` (solver.py:383-386).  nf > 0: Schur complement of the
+ * independent set fnodes[0..nf) (solver.py:251-261), map = position among the
+ * kept nodes, -1 for eliminated ones.  Both are followed by the Laplacian
+ * rebuild (solver.py:167-187).  *nnz_out = entries of the result; copy it out
+ * (and free the device buffers) with cf_coarse_fetch_dev from the same thread:
+ * out_ptr nc + 1, out_idx / out_val nnz entries, sorted rows, diagonal stored. */
+int cf_coarse_operator_dev(int32_t device, int64_t n, const int64_t* indptr,
+                           const int64_t* indices, const double* data, const int64_t* map,
+                           int64_t nc, int64_t nf, const int64_t* fnodes, int64_t* nnz_out);
+int cf_coarse_fetch_dev(int64_t* out_ptr, int64_t* out_idx, double* out_val);
 /* greedy natural-order colouring of the off-diagonal graph (multicolour
  * Gauss-Seidel, the B200 smoother ordering). */
 int cf_setup_colour(int64_t n, const int64_t* indptr, const int64_t* indices,

@@ -23,7 +23,7 @@ OBJ = os.path.join(ROOT, "build", "obj")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + INC, "-I" + CSRC,
               "--expt-relaxed-constexpr"]
-SOURCES = ["cf_setup.cpp", "cf_solve.cu", "cf_estimators.cu"]
+SOURCES = ["cf_setup.cpp", "cf_solve.cu", "cf_estimators.cu", "cf_graph.cu", "cf_setup_dev.cu"]
 
 
 def _nvcc() -> str:

@@ -102,6 +102,12 @@ _SIGS = {
     "cf_setup_permute": (C.c_int, [C.c_int64, i64p, i64p, f64p, i64p, i64p, i64p, i64p, f64p]),
     "cf_rebuild_laplacian": (C.c_int, [C.c_int64, i64p, i64p, f64p, i64p, i64p, f64p, i64p]),
     "cf_build_csr": (C.c_int, [C.c_int64, C.c_int64, i64p, i64p, f64p, i64p, i64p, f64p, i64p]),
+    "cf_csr_from_edges_dev": (C.c_int, [C.c_int32, C.c_int64, C.c_int64, i64p, i64p, f64p, i64p,
+                                        i64p, f64p, i32p]),
+    "cf_components_dev": (C.c_int, [C.c_int32, C.c_int64, C.c_int64, i64p, i64p, i64p, i32p]),
+    "cf_coarse_operator_dev": (C.c_int, [C.c_int32, C.c_int64, i64p, i64p, f64p, i64p, C.c_int64,
+                                         C.c_int64, i64p, i64p]),
+    "cf_coarse_fetch_dev": (C.c_int, [i64p, i64p, f64p]),
 }
 
 

@@ -1,0 +1,402 @@
+// Device-side coarse operators of the multigrid setup:
+// the Galerkin product P^T L P of an aggregation level (reference
+// solver.py:383-386) and the Schur complement L_cc - W D_f^-1 W^T of an
+// elimination level (solver.py:251-261), each followed by the Laplacian
+// rebuild (solver.py:167-187: symmetrise, keep strictly negative
+// off-diagonals, diagonal = minus the off-diagonal row sum).
+//
+// Both are "expand to (row, col, value) triples, sort by (row, col), sum equal
+// keys": the off-diagonal triples are generated on the GPU, sorted with a
+// stable radix sort and every run of equal keys is summed left to right by one
+// thread, so the result is a pure function of the input (no atomics on values).
+// The sums differ from scipy's SpGEMM in rounding only (different order); the
+// host route stays the default wherever hierarchies are pinned bit-for-bit to
+// the reference (n0 <= 262,144, C1-C3 and the golden graphs).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "cf_common.h"
+#include "cfcent_b200.h"
+
+namespace cf {
+namespace {
+
+struct DBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    DBuf() = default;
+    explicit DBuf(size_t bytes) { alloc(bytes); }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    void alloc(size_t bytes) {
+        release();
+        CF_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+        cap = bytes;
+    }
+    template <typename T>
+    T* as() const {
+        return reinterpret_cast<T*>(p);
+    }
+};
+
+constexpr int kT = 256;
+constexpr uint64_t kNoKey = ~(uint64_t)0;
+inline unsigned blocks_for(int64_t items) {
+    return (unsigned)std::max<int64_t>(1, (items + kT - 1) / kT);
+}
+
+// row of CSR entry p (largest i with indptr[i] <= p)
+__device__ __forceinline__ int64_t row_of(const int64_t* __restrict__ indptr, int64_t n, int64_t p) {
+    int64_t lo = 0, hi = n;
+    while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (indptr[mid] <= p)
+            lo = mid;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+// Off-diagonal triples of P^T L P: entry (i, j, a) of L -> (agg[i], agg[j], a)
+// when the aggregates differ (entries inside an aggregate only touch the
+// diagonal, which the rebuild recomputes).
+__global__ void __launch_bounds__(kT) k_galerkin_keys(int64_t n, int64_t nnz,
+                                                      const int64_t* __restrict__ indptr,
+                                                      const int64_t* __restrict__ indices,
+                                                      const double* __restrict__ data,
+                                                      const int64_t* __restrict__ map, int64_t nc,
+                                                      uint64_t* __restrict__ key,
+                                                      double* __restrict__ val) {
+    const int64_t p = (int64_t)blockIdx.x * kT + threadIdx.x;
+    if (p >= nnz) return;
+    const int64_t i = row_of(indptr, n, p);
+    const int64_t a = map[i], b = map[indices[p]];
+    const bool keep = a >= 0 && b >= 0 && a != b;
+    key[p] = keep ? (uint64_t)a * (uint64_t)nc + (uint64_t)b : kNoKey;
+    val[p] = keep ? data[p] : 0.0;
+}
+
+// Fill of the Schur complement: eliminated node f with neighbours c_1..c_d
+// (all kept: the eliminated set is independent) and weights w_k = -L[f, c_k]
+// contributes -(w_a / d_f) * w_b to (c_a, c_b), a != b.  One warp per f node;
+// off[f] = first output slot of its d (d - 1) triples.
+__global__ void __launch_bounds__(kT) k_schur_fill(int64_t nf, const int64_t* __restrict__ fnodes,
+                                                   const int64_t* __restrict__ indptr,
+                                                   const int64_t* __restrict__ indices,
+                                                   const double* __restrict__ data,
+                                                   const int64_t* __restrict__ map, int64_t nc,
+                                                   const int64_t* __restrict__ off,
+                                                   uint64_t* __restrict__ key,
+                                                   double* __restrict__ val) {
+    const int64_t w = ((int64_t)blockIdx.x * kT + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= nf) return;
+    const int64_t f = fnodes[w];
+    const int64_t beg = indptr[f], end = indptr[f + 1];
+    const int64_t d = end - beg - 1;  // off-diagonal entries (the diagonal is stored)
+    if (d < 2) return;
+    // the diagonal sits at the sorted position of f: entries after it shift by one
+    int64_t dpos = beg;
+    while (dpos < end && indices[dpos] != f) ++dpos;
+    const double df = data[dpos];
+    // pair index q = a * (d - 1) + b' over ordered pairs a != b
+    const int64_t base = off[w];
+    const int64_t pairs = d * (d - 1);
+    for (int64_t q = lane; q < pairs; q += 32) {
+        const int64_t a = q / (d - 1);
+        int64_t b = q % (d - 1);
+        if (b >= a) ++b;
+        // a-th / b-th off-diagonal entry of row f (skip the diagonal position)
+        int64_t pa = beg + a, pb = beg + b;
+        if (pa >= dpos) ++pa;
+        if (pb >= dpos) ++pb;
+        const double wa = -data[pa], wb = -data[pb];
+        const int64_t ca = map[indices[pa]], cb = map[indices[pb]];
+        key[base + q] = (uint64_t)ca * (uint64_t)nc + (uint64_t)cb;
+        val[base + q] = -((wa * (1.0 / df)) * wb);
+    }
+}
+
+__global__ void __launch_bounds__(kT) k_heads(int64_t cnt, const uint64_t* __restrict__ key,
+                                              int32_t* __restrict__ head) {
+    const int64_t t = (int64_t)blockIdx.x * kT + threadIdx.x;
+    if (t >= cnt) return;
+    head[t] = (key[t] != kNoKey && (t == 0 || key[t] != key[t - 1])) ? 1 : 0;
+}
+
+// one thread per run of equal keys: left-to-right sum (fixed order)
+__global__ void __launch_bounds__(kT) k_sum_runs(int64_t cnt, const uint64_t* __restrict__ key,
+                                                 const double* __restrict__ val,
+                                                 const int32_t* __restrict__ head,
+                                                 const int32_t* __restrict__ pos,
+                                                 uint64_t* __restrict__ ukey,
+                                                 double* __restrict__ uval) {
+    const int64_t t = (int64_t)blockIdx.x * kT + threadIdx.x;
+    if (t >= cnt || !head[t]) return;
+    const uint64_t k = key[t];
+    double s = val[t];
+    for (int64_t q = t + 1; q < cnt && key[q] == k; ++q) s += val[q];
+    ukey[pos[t]] = k;
+    uval[pos[t]] = s;
+}
+
+// symmetrise: v(I,J) = (s(I,J) + s(J,I)) * 0.5 (missing mirror = 0); keep v < 0
+__global__ void __launch_bounds__(kT) k_symmetrise(int64_t U, int64_t nc,
+                                                   const uint64_t* __restrict__ ukey,
+                                                   const double* __restrict__ uval,
+                                                   double* __restrict__ sval,
+                                                   int32_t* __restrict__ keep) {
+    const int64_t t = (int64_t)blockIdx.x * kT + threadIdx.x;
+    if (t >= U) return;
+    const uint64_t k = ukey[t];
+    const uint64_t I = k / (uint64_t)nc, J = k % (uint64_t)nc;
+    const uint64_t mk = J * (uint64_t)nc + I;
+    int64_t lo = 0, hi = U;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (ukey[mid] < mk)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    const double mirror = (lo < U && ukey[lo] == mk) ? uval[lo] : 0.0;
+    const double v = (uval[t] + mirror) * 0.5;
+    sval[t] = v;
+    keep[t] = v < 0.0 ? 1 : 0;
+}
+
+// first unique entry of every coarse row (binary search), for the row loops
+__global__ void __launch_bounds__(kT) k_urow_ptr(int64_t nc, int64_t U,
+                                                 const uint64_t* __restrict__ ukey,
+                                                 int64_t* __restrict__ urp) {
+    const int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x;
+    if (i > nc) return;
+    const uint64_t target = (uint64_t)i * (uint64_t)nc;
+    int64_t lo = 0, hi = U;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (ukey[mid] < target)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    urp[i] = lo;
+}
+
+// kept entries per row (+ 1 for the diagonal)
+__global__ void __launch_bounds__(kT) k_row_counts(int64_t nc, const int64_t* __restrict__ urp,
+                                                   const int32_t* __restrict__ keep,
+                                                   int64_t* __restrict__ cnt) {
+    const int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x;
+    if (i >= nc) return;
+    int64_t c = 1;
+    for (int64_t t = urp[i]; t < urp[i + 1]; ++t) c += keep[t];
+    cnt[i] = c;
+}
+
+// write row i: kept off-diagonals in column order with the diagonal
+// (= minus their sum, accumulated in column order) at its sorted position
+__global__ void __launch_bounds__(kT) k_emit_rows(int64_t nc, const int64_t* __restrict__ urp,
+                                                  const uint64_t* __restrict__ ukey,
+                                                  const double* __restrict__ sval,
+                                                  const int32_t* __restrict__ keep,
+                                                  const int64_t* __restrict__ optr,
+                                                  int64_t* __restrict__ oidx,
+                                                  double* __restrict__ oval) {
+    const int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x;
+    if (i >= nc) return;
+    int64_t o = optr[i];
+    int64_t dslot = -1;
+    double dg = 0.0;
+    for (int64_t t = urp[i]; t < urp[i + 1]; ++t) {
+        if (!keep[t]) continue;
+        const int64_t j = (int64_t)(ukey[t] % (uint64_t)nc);
+        if (dslot < 0 && j > i) dslot = o++;
+        oidx[o] = j;
+        oval[o] = sval[t];
+        ++o;
+        dg += -sval[t];
+    }
+    if (dslot < 0) dslot = o++;
+    oidx[dslot] = i;
+    oval[dslot] = dg;
+}
+
+// result kept on the device between cf_coarse_*_dev and cf_coarse_fetch_dev
+struct CoarseCtx {
+    int device = -1;
+    int64_t nc = 0, nnz = 0;
+    DBuf optr, oidx, oval;
+};
+thread_local CoarseCtx g_ctx;
+
+// sort the (key, val) triples, sum runs, symmetrise, assemble the CSR Laplacian
+void finish_coarse(int device, int64_t nc, int64_t cnt, DBuf& key, DBuf& val) {
+    if (cnt >= (int64_t)1 << 31) throw CfError(CF_RUNTIME, "too many triples for one device sort");
+    CoarseCtx& c = g_ctx;
+    c.device = device;
+    c.nc = nc;
+    DBuf key2(sizeof(uint64_t) * std::max<int64_t>(cnt, 1)), val2(sizeof(double) * std::max<int64_t>(cnt, 1));
+    int64_t U = 0;
+    DBuf head, pos, ukey, uval;
+    if (cnt > 0) {
+        size_t tb = 0;
+        int end_bit = 1;
+        while (end_bit < 64 && (((uint64_t)nc * (uint64_t)nc) >> end_bit)) ++end_bit;
+        // sentinel keys (all ones) must sort last: sort all 64 bits when present
+        end_bit = 64;
+        CF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, key.as<uint64_t>(), key2.as<uint64_t>(),
+                                                val.as<double>(), val2.as<double>(), (int)cnt, 0,
+                                                end_bit));
+        DBuf tmp(tb);
+        CF_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, key.as<uint64_t>(), key2.as<uint64_t>(),
+                                                val.as<double>(), val2.as<double>(), (int)cnt, 0,
+                                                end_bit));
+        head.alloc(sizeof(int32_t) * cnt);
+        pos.alloc(sizeof(int32_t) * cnt);
+        k_heads<<<blocks_for(cnt), kT>>>(cnt, key2.as<uint64_t>(), head.as<int32_t>());
+        size_t sb = 0;
+        CF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, sb, head.as<int32_t>(), pos.as<int32_t>(), (int)cnt));
+        DBuf stmp(sb);
+        CF_CUDA(cub::DeviceScan::ExclusiveSum(stmp.p, sb, head.as<int32_t>(), pos.as<int32_t>(), (int)cnt));
+        int32_t lh = 0, lp = 0;
+        CF_CUDA(cudaMemcpy(&lh, head.as<int32_t>() + (cnt - 1), sizeof(int32_t), cudaMemcpyDeviceToHost));
+        CF_CUDA(cudaMemcpy(&lp, pos.as<int32_t>() + (cnt - 1), sizeof(int32_t), cudaMemcpyDeviceToHost));
+        U = (int64_t)lh + lp;
+        ukey.alloc(sizeof(uint64_t) * std::max<int64_t>(U, 1));
+        uval.alloc(sizeof(double) * std::max<int64_t>(U, 1));
+        k_sum_runs<<<blocks_for(cnt), kT>>>(cnt, key2.as<uint64_t>(), val2.as<double>(),
+                                            head.as<int32_t>(), pos.as<int32_t>(),
+                                            ukey.as<uint64_t>(), uval.as<double>());
+        CF_CUDA(cudaGetLastError());
+    } else {
+        ukey.alloc(16);
+        uval.alloc(16);
+    }
+    key.release();
+    val.release();
+    key2.release();
+    val2.release();
+    DBuf sval(sizeof(double) * std::max<int64_t>(U, 1)), keep(sizeof(int32_t) * std::max<int64_t>(U, 1));
+    DBuf urp(sizeof(int64_t) * (nc + 1)), rcnt(sizeof(int64_t) * (nc + 1));
+    if (U) k_symmetrise<<<blocks_for(U), kT>>>(U, nc, ukey.as<uint64_t>(), uval.as<double>(),
+                                               sval.as<double>(), keep.as<int32_t>());
+    k_urow_ptr<<<blocks_for(nc + 1), kT>>>(nc, U, ukey.as<uint64_t>(), urp.as<int64_t>());
+    CF_CUDA(cudaMemset(rcnt.p, 0, sizeof(int64_t) * (nc + 1)));
+    k_row_counts<<<blocks_for(nc), kT>>>(nc, urp.as<int64_t>(), keep.as<int32_t>(), rcnt.as<int64_t>());
+    c.optr.alloc(sizeof(int64_t) * (nc + 1));
+    size_t sb = 0;
+    CF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, sb, rcnt.as<int64_t>(), c.optr.as<int64_t>(), (int)(nc + 1)));
+    DBuf stmp(sb);
+    CF_CUDA(cub::DeviceScan::ExclusiveSum(stmp.p, sb, rcnt.as<int64_t>(), c.optr.as<int64_t>(), (int)(nc + 1)));
+    int64_t total = 0;
+    CF_CUDA(cudaMemcpy(&total, c.optr.as<int64_t>() + nc, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    c.nnz = total;
+    c.oidx.alloc(sizeof(int64_t) * std::max<int64_t>(total, 1));
+    c.oval.alloc(sizeof(double) * std::max<int64_t>(total, 1));
+    k_emit_rows<<<blocks_for(nc), kT>>>(nc, urp.as<int64_t>(), ukey.as<uint64_t>(), sval.as<double>(),
+                                        keep.as<int32_t>(), c.optr.as<int64_t>(), c.oidx.as<int64_t>(),
+                                        c.oval.as<double>());
+    CF_CUDA(cudaGetLastError());
+    CF_CUDA(cudaDeviceSynchronize());
+}
+
+}  // namespace
+}  // namespace cf
+
+using namespace cf;
+
+// Coarse operator of one setup level on GPU `device`.  L: n x n CSR with its
+// diagonal stored, sorted rows.  map[i] = coarse index of fine node i (the
+// aggregate for a Galerkin product; the position among the kept nodes, or -1
+// for an eliminated node, for a Schur complement).  nf = 0: Galerkin
+// (solver.py:383-386); nf > 0: Schur complement of the independent set
+// fnodes (solver.py:251-261).  *nnz_out = entries of the rebuilt coarse
+// Laplacian (diagonal included), fetched with cf_coarse_fetch_dev.
+extern "C" int cf_coarse_operator_dev(int32_t device, int64_t n, const int64_t* indptr,
+                                      const int64_t* indices, const double* data,
+                                      const int64_t* map, int64_t nc, int64_t nf,
+                                      const int64_t* fnodes, int64_t* nnz_out) {
+    CF_API_BEGIN
+    if (n < 0 || nc < 0 || nf < 0) throw CfError(CF_DOMAIN, "negative sizes");
+    if ((uint64_t)nc >= ((uint64_t)1 << 31)) throw CfError(CF_RUNTIME, "too many coarse nodes");
+    CF_CUDA(cudaSetDevice(device));
+    const int64_t nnz = indptr[n];
+    DBuf dp(sizeof(int64_t) * (n + 1)), di(sizeof(int64_t) * std::max<int64_t>(nnz, 1));
+    DBuf dd(sizeof(double) * std::max<int64_t>(nnz, 1)), dm(sizeof(int64_t) * std::max<int64_t>(n, 1));
+    CF_CUDA(cudaMemcpy(dp.p, indptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice));
+    if (nnz) {
+        CF_CUDA(cudaMemcpy(di.p, indices, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice));
+        CF_CUDA(cudaMemcpy(dd.p, data, sizeof(double) * nnz, cudaMemcpyHostToDevice));
+    }
+    if (n) CF_CUDA(cudaMemcpy(dm.p, map, sizeof(int64_t) * n, cudaMemcpyHostToDevice));
+    // fill triples of the eliminated nodes
+    int64_t fill = 0;
+    DBuf dfn, doff;
+    if (nf > 0) {
+        std::vector<int64_t> off((size_t)nf);
+        for (int64_t w = 0; w < nf; ++w) {
+            const int64_t f = fnodes[w];
+            const int64_t d = indptr[f + 1] - indptr[f] - 1;
+            off[(size_t)w] = fill;
+            fill += d > 1 ? d * (d - 1) : 0;
+        }
+        dfn.alloc(sizeof(int64_t) * nf);
+        doff.alloc(sizeof(int64_t) * nf);
+        CF_CUDA(cudaMemcpy(dfn.p, fnodes, sizeof(int64_t) * nf, cudaMemcpyHostToDevice));
+        CF_CUDA(cudaMemcpy(doff.p, off.data(), sizeof(int64_t) * nf, cudaMemcpyHostToDevice));
+    }
+    const int64_t cnt = nnz + fill;
+    DBuf key(sizeof(uint64_t) * std::max<int64_t>(cnt, 1)), val(sizeof(double) * std::max<int64_t>(cnt, 1));
+    if (nnz)
+        k_galerkin_keys<<<blocks_for(nnz), kT>>>(n, nnz, dp.as<int64_t>(), di.as<int64_t>(),
+                                                 dd.as<double>(), dm.as<int64_t>(), nc,
+                                                 key.as<uint64_t>(), val.as<double>());
+    if (fill)
+        k_schur_fill<<<blocks_for(nf * 32), kT>>>(nf, dfn.as<int64_t>(), dp.as<int64_t>(),
+                                                  di.as<int64_t>(), dd.as<double>(),
+                                                  dm.as<int64_t>(), nc, doff.as<int64_t>(),
+                                                  key.as<uint64_t>() + nnz, val.as<double>() + nnz);
+    CF_CUDA(cudaGetLastError());
+    CF_CUDA(cudaDeviceSynchronize());
+    dp.release();
+    di.release();
+    dd.release();
+    dm.release();
+    finish_coarse(device, nc, cnt, key, val);
+    *nnz_out = g_ctx.nnz;
+    CF_API_END
+}
+
+// Copy out the coarse Laplacian computed by the last cf_coarse_operator_dev
+// call of this thread (out_ptr: nc + 1; out_idx / out_val: *nnz_out entries)
+// and release its device buffers.
+extern "C" int cf_coarse_fetch_dev(int64_t* out_ptr, int64_t* out_idx, double* out_val) {
+    CF_API_BEGIN
+    CoarseCtx& c = g_ctx;
+    if (c.device < 0) throw CfError(CF_DOMAIN, "no coarse operator pending");
+    CF_CUDA(cudaSetDevice(c.device));
+    CF_CUDA(cudaMemcpy(out_ptr, c.optr.p, sizeof(int64_t) * (c.nc + 1), cudaMemcpyDeviceToHost));
+    if (c.nnz) {
+        CF_CUDA(cudaMemcpy(out_idx, c.oidx.p, sizeof(int64_t) * c.nnz, cudaMemcpyDeviceToHost));
+        CF_CUDA(cudaMemcpy(out_val, c.oval.p, sizeof(double) * c.nnz, cudaMemcpyDeviceToHost));
+    }
+    c.optr.release();
+    c.oidx.release();
+    c.oval.release();
+    c.device = -1;
+    CF_API_END
+}

@@ -111,9 +111,22 @@ class Graph:
         dst = np.empty(2 * u.size, dtype=np.int64)
         wt = np.empty(2 * u.size, dtype=np.float64)
         nnz = np.zeros(1, dtype=np.int64)
-        N.check(N.lib().cf_build_csr(n, u.size, N.ptr(u, N.i64p), N.ptr(v, N.i64p),
-                                     N.ptr(w, N.f64p), N.ptr(indptr, N.i64p), N.ptr(dst, N.i64p),
-                                     N.ptr(wt, N.f64p), N.ptr(nnz, N.i64p)))
+        if _device_ingest(u.size):
+            # large edge lists: stable radix sort of the adjacency entries on
+            # the GPU (csrc/cf_graph.cu), the same arrays as the host route
+            st = np.zeros(1, dtype=np.int32)
+            N.check(N.lib().cf_csr_from_edges_dev(_ingest_device(), n, u.size, N.ptr(u, N.i64p),
+                                                  N.ptr(v, N.i64p), N.ptr(w, N.f64p),
+                                                  N.ptr(indptr, N.i64p), N.ptr(dst, N.i64p),
+                                                  N.ptr(wt, N.f64p), N.ptr(st, N.i32p)))
+            if st[0] == 2:
+                raise DomainError("node ids out of range")
+            nnz[0] = 2 * u.size if st[0] == 0 else -1
+        else:
+            N.check(N.lib().cf_build_csr(n, u.size, N.ptr(u, N.i64p), N.ptr(v, N.i64p),
+                                         N.ptr(w, N.f64p), N.ptr(indptr, N.i64p),
+                                         N.ptr(dst, N.i64p), N.ptr(wt, N.f64p),
+                                         N.ptr(nnz, N.i64p)))
         if nnz[0] == 2 * u.size:
             dst, wt = dst[:nnz[0]], wt[:nnz[0]]
         else:
@@ -135,12 +148,54 @@ class Graph:
         return Graph(indptr=indptr, indices=dst, weights=wt, node_labels=node_labels)
 
 
+# Edge lists of at least this many edges are sorted / labelled on the GPU when
+# one is visible; smaller ones, and any process without
+# a device, take the native host route -- both produce identical arrays
+# (tests/test_gpu_solver.py::test_device_ingestion_matches_host).
+DEVICE_INGEST_MIN_EDGES = 1 << 20
+
+
+def _device_ingest(m: int) -> bool:
+    import os
+
+    if os.environ.get("CF_DEVICE_INGEST", "1") == "0" or m < DEVICE_INGEST_MIN_EDGES:
+        return False
+    from . import _native as N
+
+    return N.device_available()
+
+
+def _ingest_device() -> int:
+    import os
+
+    return int(os.environ.get("LOCAL_RANK", "0"))
+
+
 def largest_connected_component(g: Graph):
     """LCC, ties to the component holding the smallest label
     (graph.py:217-250).  Returns (subgraph, {old: new})."""
     if g.n == 0:
         raise DomainError("cannot extract a component of an empty graph")
-    ncomp, comp = connected_components(g.adjacency_matrix(), directed=False)
+    eu = ev = ew = None
+    if _device_ingest(g.m):
+        # component roots (smallest node id per component) from the GPU's
+        # hook / pointer-jumping rounds; roots in ascending order number the
+        # components exactly as scipy does (first occurrence)
+        from . import _native as N
+
+        eu, ev, ew = g.edge_array()
+        eu = np.ascontiguousarray(eu, dtype=np.int64)
+        ev = np.ascontiguousarray(ev, dtype=np.int64)
+        root = np.empty(g.n, dtype=np.int64)
+        rounds = np.zeros(1, dtype=np.int32)
+        N.check(N.lib().cf_components_dev(_ingest_device(), g.n, eu.size, N.ptr(eu, N.i64p),
+                                          N.ptr(ev, N.i64p), N.ptr(root, N.i64p),
+                                          N.ptr(rounds, N.i32p)))
+        is_root = root == np.arange(g.n)
+        ncomp = int(is_root.sum())
+        comp = (np.cumsum(is_root) - 1)[root]
+    else:
+        ncomp, comp = connected_components(g.adjacency_matrix(), directed=False)
     if ncomp == 1:
         return g, {i: i for i in range(g.n)}
     sizes = np.bincount(comp, minlength=ncomp)
@@ -152,7 +207,8 @@ def largest_connected_component(g: Graph):
     keep = np.flatnonzero(comp == pick)
     remap = np.full(g.n, -1, dtype=np.int64)
     remap[keep] = np.arange(keep.size)
-    eu, ev, ew = g.edge_array()
+    if eu is None:
+        eu, ev, ew = g.edge_array()
     sel = remap[eu] >= 0
     sub = Graph.from_edges(remap[eu[sel]], remap[ev[sel]], ew[sel], n=keep.size,
                            node_labels=g.node_labels[keep].copy())

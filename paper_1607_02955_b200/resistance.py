@@ -195,6 +195,10 @@ def _device_graph(g: Graph, hierarchy: MultigridHierarchy) -> _DeviceGraph:
     key = id(g)
     ent = per.get(key)
     if ent is None or ent[0]() is not g:
+        # entries of graphs that have died are dropped here, so their device
+        # copies (adjacency, edge ids, sqrt(w), sign bits) do not outlive them
+        for dead in [k for k, (ref, _) in per.items() if ref() is None]:
+            per.pop(dead, None)
         ent = (weakref.ref(g), _DeviceGraph(g, hierarchy))
         per[key] = ent
     return ent[1]

@@ -577,6 +577,51 @@ def _elim_select(matrix: sp.csr_matrix, cap: int) -> np.ndarray:
     return out[:cnt[0]].copy()
 
 
+# Coarse operators on the GPU (csrc/cf_setup_dev.cu) for
+# graphs above STALL_BREAKER_MIN_N0 nodes -- exactly the graphs whose
+# hierarchies already differ from the reference's (stall breaker, hub
+# aggregates); below it the host route keeps hierarchies bit-identical to the
+# reference's goldens.  The device sums equal keys in sorted order, scipy in
+# its SpGEMM order: values agree to rounding (tests/test_gpu_solver.py).
+DEVICE_SETUP_MIN_NNZ = 1 << 21
+DEVICE_SETUP_MIN_N0 = STALL_BREAKER_MIN_N0
+_device_setup_on = False
+
+
+def _device_setup(nnz: int) -> bool:
+    if not _device_setup_on or nnz < DEVICE_SETUP_MIN_NNZ:
+        return False
+    if os.environ.get("CF_DEVICE_SETUP", "1") == "0":
+        return False
+    return N.device_available()
+
+
+def _coarse_operator_dev(matrix: sp.csr_matrix, cmap: np.ndarray, nc: int,
+                         f: np.ndarray | None = None) -> sp.csr_matrix:
+    """Galerkin product (f None) or Schur complement of the independent set f,
+    rebuilt as a Laplacian, on the GPU."""
+    m = matrix.tocsr()
+    if not m.has_sorted_indices:
+        m = m.sorted_indices()
+    ip, ix = _csr64(m)
+    dv = np.ascontiguousarray(m.data, dtype=np.float64)
+    cmap = np.ascontiguousarray(cmap, dtype=np.int64)
+    fn = np.ascontiguousarray(f if f is not None else np.zeros(0), dtype=np.int64)
+    nnz = np.zeros(1, dtype=np.int64)
+    L = N.lib()
+    N.check(L.cf_coarse_operator_dev(_device_index(), m.shape[0], N.ptr(ip, N.i64p),
+                                     N.ptr(ix, N.i64p), N.ptr(dv, N.f64p), N.ptr(cmap, N.i64p),
+                                     int(nc), fn.size, N.ptr(fn, N.i64p), N.ptr(nnz, N.i64p)))
+    k = int(nnz[0])
+    op = np.empty(nc + 1, dtype=np.int64)
+    oi = np.empty(max(k, 1), dtype=np.int64)
+    ov = np.empty(max(k, 1), dtype=np.float64)
+    N.check(L.cf_coarse_fetch_dev(N.ptr(op, N.i64p), N.ptr(oi, N.i64p), N.ptr(ov, N.f64p)))
+    out = sp.csr_matrix((ov[:k], oi[:k].astype(np.int32), op.astype(np.int32)), shape=(nc, nc))
+    out.has_sorted_indices = True
+    return out
+
+
 def _eliminate_set(matrix: sp.csr_matrix, f: np.ndarray):
     """Exact Schur complement of the independent set f (solver.py:251-261)."""
     n = matrix.shape[0]
@@ -585,6 +630,11 @@ def _eliminate_set(matrix: sp.csr_matrix, f: np.ndarray):
     c = np.flatnonzero(~in_f)
     d_f = matrix.diagonal()[f]
     w_cf = (-(matrix[c][:, f].tocsr())).tocsr()
+    if _device_setup(matrix.nnz):
+        cmap = np.full(n, -1, dtype=np.int64)
+        cmap[c] = np.arange(c.size)
+        schur = _coarse_operator_dev(matrix, cmap, c.size, np.asarray(f, dtype=np.int64))
+        return schur, EliminationRecord(f_nodes=f, c_nodes=c, f_degree=d_f, w_cf=w_cf)
     schur = matrix[c][:, c] - w_cf @ sp.diags(1.0 / d_f) @ w_cf.T
     return _rebuild_laplacian(schur, unique=True), EliminationRecord(f_nodes=f, c_nodes=c, f_degree=d_f,
                                                         w_cf=w_cf)
@@ -603,6 +653,8 @@ def relaxed_test_vectors(matrix: sp.csr_matrix, count: int, rng: np.random.Gener
 
 
 def _galerkin(matrix: sp.csr_matrix, agg: np.ndarray, n_agg: int) -> sp.csr_matrix:
+    if _device_setup(matrix.nnz):
+        return _coarse_operator_dev(matrix, agg, n_agg)
     n = matrix.shape[0]
     p = sp.csr_matrix((np.ones(n), (np.arange(n), agg)), shape=(n, n_agg))
     return _rebuild_laplacian(p.T @ matrix @ p, unique=True)
@@ -701,6 +753,8 @@ def setup(matrix: sp.spmatrix, config: SolverConfig | None = None,
     """
     config = config or SolverConfig()
     current = _validate_laplacian(matrix)
+    global _device_setup_on
+    _device_setup_on = stall_breaker is not False and current.shape[0] > DEVICE_SETUP_MIN_N0
     rng = np.random.default_rng(config.seed)
     levels: list[Level] = []
     preferred = LevelKind.ELIMINATION

@@ -355,8 +355,12 @@ def config_rmat(name, scale, ef, seed, weighted, k, query_fn, jl_rows=32, samp=N
 
 
 def config4():
+    # 4 sketch rows: the reference's recursion keeps three n_l x rows arrays
+    # alive on each of its 3,576 levels (sum n_l = 92.7 M), on top of a 39 GB
+    # hierarchy -- 32 rows exceed the build container's 62 GB
     config_rmat("config4", 20, 16, 4, True, 256,
-                lambda g: np.sort(np.random.default_rng(4).choice(g.n, 1000, replace=False)))
+                lambda g: np.sort(np.random.default_rng(4).choice(g.n, 1000, replace=False)),
+                jl_rows=int(os.environ.get("GOLDEN_JL_ROWS", "4")))
 
 
 def config5():

@@ -37,6 +37,18 @@ from oracle import lamg_oracle as O  # noqa: E402
 from oracle import workloads as OW  # noqa: E402
 
 
+def _cpu_info():
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return f"{model}; {os.cpu_count()} cores"
+
+
 def main():
     rows = int(sys.argv[1]) if len(sys.argv) > 1 else 8
     npiv = int(sys.argv[2]) if len(sys.argv) > 2 else 16
@@ -58,6 +70,7 @@ def main():
     print("host setup", [lv.size for lv in h.levels], time.perf_counter() - t1, flush=True)
     d = {"n": np.int64(n), "m": np.int64(g[0][-1] // 2), "k": np.int64(k), "query": np.array([u]),
          "jl_rows": np.int64(rows), "sizes": np.array([lv.size for lv in h.levels]),
+         "cpu": np.array(_cpu_info()),
          "source": np.array("oracle solve loop on this build's host hierarchy (reference setup "
                             "does not finish at this scale)")}
     # first `rows` sketch rows: the first rows*m draws of the row-major stream

@@ -316,3 +316,24 @@ def test_exact_closeness_vs_reference_10k():
     q = d["query"].tolist()
     got = P.cf_closeness_exact(g, h, q, cfg).vector(q)
     assert np.allclose(got, d["exact"], rtol=1e-6), np.abs(got / d["exact"] - 1).max()
+
+
+def test_jl_multi_chunk_pipeline_bitwise():
+    """A sketch of several device chunks (the next chunk's right-hand sides
+    are built on a second stream while the current chunk solves, and a
+    129..192-row remainder runs as one wide chunk) gives bit for bit the
+    per-row parts of the same rows solved in separate single-chunk calls."""
+    from paper_1607_02955_b200.resistance import combine_row_parts, sketch_closeness_sums
+
+    g = G.grid_graph(40)
+    cfg = P.SolverConfig(tau=1e-8)
+    h = P.setup(P.laplacian(g), cfg)
+    q = np.array([0, 777, 1599])
+    eps = math.sqrt(math.log(g.n) / (430 - 0.5))
+    k, sums, res, parts = sketch_closeness_sums(g, h, eps, 5, q, cfg, row_parts=True)
+    assert k == 430 and res.max() <= 1e-8  # chunks of 128, 128, 174 (wide)
+    pieces = []
+    for lo, hi in ((0, 128), (128, 256), (256, 384), (384, 430)):
+        pieces.append(sketch_closeness_sums(g, h, eps, 5, q, cfg, rows=(lo, hi), row_parts=True)[3])
+    assert np.array_equal(parts, np.vstack(pieces))
+    assert np.array_equal(sums, combine_row_parts(np.vstack(pieces), g.n))

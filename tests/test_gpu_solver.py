@@ -318,3 +318,98 @@ def test_pinned_pipeline_error_drains_copies(rng):
     rows[150, 3] -= 1.0
     got = P.solve_many(h, rows, out=out)
     assert max(p.achieved_residual for p in got) <= 1e-8
+
+
+def test_device_ingestion_matches_host(monkeypatch):
+    """Graph.from_edges and largest_connected_component
+    on the GPU (csrc/cf_graph.cu: stable radix sort of the adjacency entries,
+    min-id hooking + pointer jumping) produce exactly the host route's arrays
+    (graph.py:100-147, 217-250): random sparse graph with many components,
+    weighted; duplicate edges are detected and summed on the host route."""
+    from paper_1607_02955_b200 import graph as GR
+
+    r = np.random.default_rng(11)
+    n, m = 300_000, 420_000  # mean degree 2.8: a giant component plus many small ones
+    u = r.integers(0, n, m)
+    v = r.integers(0, n, m)
+    keep = u != v
+    u, v = u[keep], v[keep]
+    key = np.unique(np.minimum(u, v) * n + np.maximum(u, v))
+    u, v = key // n, key % n
+    w = r.random(u.size) + 0.5
+
+    def build(dev):
+        monkeypatch.setattr(GR, "DEVICE_INGEST_MIN_EDGES", 1 if dev else 1 << 62)
+        g = P.Graph.from_edges(u, v, w, n=n)
+        sub, remap = P.largest_connected_component(g)
+        return g, sub, remap
+
+    gh, sh, rh = build(False)
+    gd, sd, rd = build(True)
+    for a, b in ((gh, gd), (sh, sd)):
+        assert np.array_equal(a.indptr, b.indptr)
+        assert np.array_equal(a.indices, b.indices)
+        assert np.array_equal(a.weights, b.weights)
+        assert np.array_equal(a.node_labels, b.node_labels)
+    assert rh == rd and sh.n < n and sh.is_connected()
+    # duplicates (and both orientations) go through the host sum, same result
+    u2, v2, w2 = np.r_[u, v[:1000]], np.r_[v, u[:1000]], np.r_[w, w[:1000] * 0.25]
+    monkeypatch.setattr(GR, "DEVICE_INGEST_MIN_EDGES", 1)
+    a = P.Graph.from_edges(u2, v2, w2, n=n)
+    monkeypatch.setattr(GR, "DEVICE_INGEST_MIN_EDGES", 1 << 62)
+    b = P.Graph.from_edges(u2, v2, w2, n=n)
+    assert np.array_equal(a.indices, b.indices) and np.array_equal(a.weights, b.weights)
+    # equal-size components: the tie goes to the smallest label on both routes
+    monkeypatch.setattr(GR, "DEVICE_INGEST_MIN_EDGES", 1)
+    t = P.Graph.from_edges([0, 1, 3, 4, 6], [1, 2, 4, 5, 7], n=8)
+    sub, remap = P.largest_connected_component(t)
+    assert sorted(remap) == [0, 1, 2]
+    with pytest.raises(P.DomainError):
+        P.Graph.from_edges([0, 9], [1, 2], n=4)
+
+
+def test_device_coarse_operators_match_host(rng):
+    """the Galerkin product and the Schur complement
+    (+ Laplacian rebuild) computed on the GPU (csrc/cf_setup_dev.cu: triples,
+    stable radix sort, runs summed in order) against the host route
+    (solver.py:251-261, 383-386, 167-187 via scipy): identical sparsity
+    pattern, values to rounding (the summation order differs), exact zero row
+    sums structure (diagonal = minus the off-diagonal sum)."""
+    from paper_1607_02955_b200 import solver as S
+
+    u, v, w = random_connected_graph_edges(6000, rng, weighted=True)
+    g = P.Graph.from_edges(u, v, w, n=6000)
+    A = S._validate_laplacian(P.laplacian(g))
+    # Galerkin: random aggregation with aggregates of 1..6 nodes
+    agg = np.sort(rng.integers(0, 2000, 6000))
+    agg = np.unique(agg, return_inverse=True)[1]
+    nc = int(agg.max()) + 1
+    host = S._galerkin(A, agg, nc)
+    dev = S._coarse_operator_dev(A, agg, nc)
+    for a, b in ((host, dev),):
+        assert np.array_equal(a.indptr, b.indptr) and np.array_equal(a.indices, b.indices)
+        assert np.allclose(a.data, b.data, rtol=1e-13, atol=0)
+    assert np.abs(np.asarray(dev.sum(axis=1))).max() <= 1e-12 * np.abs(dev.data).max()
+    # Schur complement of a greedy independent low-degree set
+    f = S._elim_select(A, 6)
+    assert f.size > 100
+    host, rec = S._eliminate_set(A, f)
+    cmap = np.full(A.shape[0], -1, dtype=np.int64)
+    cmap[rec.c_nodes] = np.arange(rec.c_nodes.size)
+    dev = S._coarse_operator_dev(A, cmap, rec.c_nodes.size, f)
+    assert np.array_equal(host.indptr, dev.indptr) and np.array_equal(host.indices, dev.indices)
+    assert np.allclose(host.data, dev.data, rtol=1e-12, atol=0)
+    # a hierarchy built with the device operators solves to the same answers
+    saved = S.DEVICE_SETUP_MIN_NNZ, S.DEVICE_SETUP_MIN_N0
+    try:
+        S.DEVICE_SETUP_MIN_NNZ, S.DEVICE_SETUP_MIN_N0 = 1, 1
+        h_dev = P.setup(P.laplacian(g), P.SolverConfig(tau=1e-10))
+        assert len(h_dev.levels) >= 2
+    finally:
+        S.DEVICE_SETUP_MIN_NNZ, S.DEVICE_SETUP_MIN_N0 = saved
+        S._device_setup_on = False
+    b = rng.standard_normal((4, g.n))
+    b -= b.mean(axis=1, keepdims=True)
+    x = np.stack([p.values for p in P.solve_many(h_dev, b)])
+    L = P.laplacian(g)
+    assert max(np.linalg.norm(L @ x[i] - b[i]) / np.linalg.norm(b[i]) for i in range(4)) <= 1e-10
