@@ -444,7 +444,23 @@ template <int KC>
 __device__ __forceinline__ void heavy_partials(const HeavyDev& H, int hv, int c0,
                                                DV<Lay<KC>::VEC>& acc) {
     constexpr int V = Lay<KC>::VEC;
-    for (int64_t sgi = H.hsp[hv]; sgi < H.hsp[hv + 1]; ++sgi) {
+    // a hub row has thousands of partials and one warp sums them: keep NB
+    // loads in flight (same register budget as the gather loop); the adds stay
+    // in segment order
+    constexpr int NB0 = CF_GATHER_DOUBLES / V > 0 ? CF_GATHER_DOUBLES / V : 1;
+    constexpr int NB = NB0 > 8 ? 8 : NB0;
+    const int64_t s0 = H.hsp[hv], s1 = H.hsp[hv + 1];
+    int64_t sgi = s0;
+    for (; sgi + NB <= s1; sgi += NB) {
+        DV<V> q[NB];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) q[b] = ldv<V>(H.P + (size_t)(sgi + b) * KC + c0);
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+#pragma unroll
+            for (int t = 0; t < V; ++t) acc.v[t] += q[b].v[t];
+    }
+    for (; sgi < s1; ++sgi) {
         DV<V> q = ldv<V>(H.P + (size_t)sgi * KC + c0);
 #pragma unroll
         for (int t = 0; t < V; ++t) acc.v[t] += q.v[t];
@@ -467,11 +483,7 @@ __device__ __forceinline__ void row_sum_from(const HeavyDev& H, int64_t i,
     // row-to-heavy-index lookup is only paid by heavy rows
     const int hv = (H.hv && end - beg > kHeavyNnz) ? H.hv[i] : -1;
     if (hv >= 0) {
-        for (int64_t sgi = H.hsp[hv]; sgi < H.hsp[hv + 1]; ++sgi) {
-            DV<V> q = ldv<V>(H.P + (size_t)sgi * KC + c0);
-#pragma unroll
-            for (int t = 0; t < V; ++t) acc.v[t] += q.v[t];
-        }
+        heavy_partials<KC>(H, hv, c0, acc);
     } else {
         gather_row_from<KC, MODE>(col, val, beg, end, map, div, X, c0, acc, jj, aa, dd);
     }

@@ -2442,7 +2442,14 @@ static Plan build_plan(Hier& h, int64_t n, const int64_t* rp, const int32_t* ord
         if (windows) {
             // processing orders: stable sort by the window of the first entry
             std::vector<int32_t> key((size_t)pl.nseg), ord((size_t)pl.nseg);
-            for (int64_t sgi = 0; sgi < pl.nseg; ++sgi) key[(size_t)sgi] = (int32_t)(col[sb[(size_t)sgi]] / W);
+            // CF_SEG_SORT=col: order by first column (finer than the window: the
+            // warps of a CTA then start at neighbouring columns)
+            static const bool by_col = [] {
+                const char* e = std::getenv("CF_SEG_SORT");
+                return e && std::string(e) == "col";
+            }();
+            for (int64_t sgi = 0; sgi < pl.nseg; ++sgi)
+                key[(size_t)sgi] = by_col ? col[sb[(size_t)sgi]] : (int32_t)(col[sb[(size_t)sgi]] / W);
             auto sort_range = [&](int64_t a, int64_t b) {
                 for (int64_t t = a; t < b; ++t) ord[(size_t)t] = (int32_t)t;
                 std::stable_sort(ord.begin() + a, ord.begin() + b,

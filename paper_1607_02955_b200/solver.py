@@ -578,10 +578,11 @@ def _elim_select(matrix: sp.csr_matrix, cap: int) -> np.ndarray:
 
 
 # Coarse operators on the GPU (csrc/cf_setup_dev.cu) for
-# graphs above STALL_BREAKER_MIN_N0 nodes -- exactly the graphs whose
-# hierarchies already differ from the reference's (stall breaker, hub
-# aggregates); below it the host route keeps hierarchies bit-identical to the
-# reference's goldens.  The device sums equal keys in sorted order, scipy in
+# hub graphs above STALL_BREAKER_MIN_N0 nodes (maximum degree > HUB_DEGREE_RATIO
+# x the mean on the finest level) -- exactly the graphs whose hierarchies
+# already differ from the reference's (stall breaker, hub aggregates);
+# everywhere else the host route keeps hierarchies bit-identical to the
+# reference's goldens (C1-C3).  The device sums equal keys in sorted order, scipy in
 # its SpGEMM order: values agree to rounding (tests/test_gpu_solver.py).
 DEVICE_SETUP_MIN_NNZ = 1 << 21
 DEVICE_SETUP_MIN_N0 = STALL_BREAKER_MIN_N0
@@ -754,7 +755,7 @@ def setup(matrix: sp.spmatrix, config: SolverConfig | None = None,
     config = config or SolverConfig()
     current = _validate_laplacian(matrix)
     global _device_setup_on
-    _device_setup_on = stall_breaker is not False and current.shape[0] > DEVICE_SETUP_MIN_N0
+    _device_setup_on = False
     rng = np.random.default_rng(config.seed)
     levels: list[Level] = []
     preferred = LevelKind.ELIMINATION
@@ -770,6 +771,12 @@ def setup(matrix: sp.spmatrix, config: SolverConfig | None = None,
             return False
         offdeg = np.diff(mat.indptr) - 1
         return offdeg.max() > HUB_DEGREE_RATIO * max(offdeg.mean(), 1.0)
+    # device coarse operators only on hub graphs (power-law: their hierarchies
+    # already differ from the reference's); C3-like graphs keep the host
+    # products and with them hierarchies identical to the reference's
+    if stall_breaker is not False and n0 > DEVICE_SETUP_MIN_N0:
+        od0 = np.diff(current.indptr) - 1
+        _device_setup_on = bool(od0.max() > HUB_DEGREE_RATIO * max(od0.mean(), 1.0))
     while current.shape[0] > config.max_direct_size:
         n_cur = current.shape[0]
         need = MIN_REDUCTION * n_cur

@@ -319,6 +319,8 @@ def config_rmat(name, scale, ef, seed, weighted, k, query_fn, jl_rows=32, samp=N
         h = slv.setup(cfcent.laplacian(g), cfg0)
         t_setup = time.perf_counter() - t1
         try:
+            if os.environ.get("GOLDEN_NO_CACHE"):
+                raise RuntimeError("GOLDEN_NO_CACHE set")
             import pickle
             os.makedirs(os.path.dirname(cache), exist_ok=True)
             with open(cache, "wb") as f:

@@ -377,8 +377,12 @@ def test_device_coarse_operators_match_host(rng):
     sums structure (diagonal = minus the off-diagonal sum)."""
     from paper_1607_02955_b200 import solver as S
 
-    u, v, w = random_connected_graph_edges(6000, rng, weighted=True)
-    g = P.Graph.from_edges(u, v, w, n=6000)
+    n = 6000  # sparse connected graph: a path plus 2n random edges (mean degree ~6)
+    ru, rv = rng.integers(0, n, 2 * n), rng.integers(0, n, 2 * n)
+    keep = ru != rv
+    u = np.r_[np.arange(n - 1), ru[keep]]
+    v = np.r_[np.arange(1, n), rv[keep]]
+    g = P.Graph.from_edges(u, v, rng.random(u.size) + 0.5, n=n)
     A = S._validate_laplacian(P.laplacian(g))
     # Galerkin: random aggregation with aggregates of 1..6 nodes
     agg = np.sort(rng.integers(0, 2000, 6000))
@@ -400,13 +404,13 @@ def test_device_coarse_operators_match_host(rng):
     assert np.array_equal(host.indptr, dev.indptr) and np.array_equal(host.indices, dev.indices)
     assert np.allclose(host.data, dev.data, rtol=1e-12, atol=0)
     # a hierarchy built with the device operators solves to the same answers
-    saved = S.DEVICE_SETUP_MIN_NNZ, S.DEVICE_SETUP_MIN_N0
+    saved = S.DEVICE_SETUP_MIN_NNZ, S.DEVICE_SETUP_MIN_N0, S.HUB_DEGREE_RATIO
     try:
-        S.DEVICE_SETUP_MIN_NNZ, S.DEVICE_SETUP_MIN_N0 = 1, 1
+        S.DEVICE_SETUP_MIN_NNZ, S.DEVICE_SETUP_MIN_N0, S.HUB_DEGREE_RATIO = 1, 1, 0.0
         h_dev = P.setup(P.laplacian(g), P.SolverConfig(tau=1e-10))
-        assert len(h_dev.levels) >= 2
+        assert S._device_setup_on and len(h_dev.levels) >= 2
     finally:
-        S.DEVICE_SETUP_MIN_NNZ, S.DEVICE_SETUP_MIN_N0 = saved
+        S.DEVICE_SETUP_MIN_NNZ, S.DEVICE_SETUP_MIN_N0, S.HUB_DEGREE_RATIO = saved
         S._device_setup_on = False
     b = rng.standard_normal((4, g.n))
     b -= b.mean(axis=1, keepdims=True)

@@ -53,6 +53,13 @@ for j, (kind, a) in enumerate(mats):
         print(f"   thr {thr:5d}: heavy rows {hv.sum():7d} nnz HH {np.mean(hr & hc):.3f} "
               f"HL {np.mean(hr & ~hc):.3f} LH {np.mean(~hr & hc):.3f} LL {np.mean(~hr & ~hc):.3f}")
     order = np.argsort(-deg, kind="stable")
+    for top in (1024, 4096, 16384):
+        if top < n:
+            intop = np.zeros(n, dtype=bool)
+            intop[order[:top]] = True
+            blk = int(np.sum(intop[rows] & intop[cols]))
+            print(f"   top {top:6d} x {top:6d} block: {blk} nnz = {blk / nnz:.3f} of the level, "
+                  f"{blk / (top * top):.3f} full")
     cum = np.cumsum(deg[order]) / nnz
     for top in (4096, 16384, 32768, 65536, 131072):
         if top < n:
