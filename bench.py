@@ -584,6 +584,10 @@ def run_gpu_arm(args):
                          "gather_bytes_per_launch": ginst[dom_name] / dom_la,
                          "gather_gbs": ginst[dom_name] / dom_la / (dom_ms_per_launch * 1e-3) / 1e9,
                          "l2_ref_gbs": L2_REF_GBS,
+                         # the bound that binds the hub-level gathers:
+                         # gather volume over the L2 -> SM throughput reference
+                         "l2_frac": (ginst[dom_name] / dom_la / (dom_ms_per_launch * 1e-3) / 1e9
+                                     / L2_REF_GBS),
                          "l2_ref_source": "B300_MICROARCH.md LTS cap ~6300 B/clk x 1.965 GHz "
                                           "(B300-measured; B200 assumed similar)",
                          # measured DRAM bytes over the SAME launch's ncu duration

@@ -250,6 +250,13 @@ int cf_coarse_operator_dev(int32_t device, int64_t n, const int64_t* indptr,
                            const int64_t* indices, const double* data, const int64_t* map,
                            int64_t nc, int64_t nf, const int64_t* fnodes, int64_t* nnz_out);
 int cf_coarse_fetch_dev(int64_t* out_ptr, int64_t* out_idx, double* out_val);
+/* The checks of _validate_laplacian (solver.py:190-211) on the GPU for an n x n
+ * CSR with sorted rows: out[0] = max |entry|, out[1] = max |m - m^T|,
+ * out[2] = max |row sum|, out[3] = largest positive off-diagonal (0 if none);
+ * *ncomp = connected components of the pattern. */
+int cf_validate_laplacian_dev(int32_t device, int64_t n, const int64_t* indptr,
+                              const int64_t* indices, const double* data, double* out,
+                              int64_t* ncomp);
 /* greedy natural-order colouring of the off-diagonal graph (multicolour
  * Gauss-Seidel, the B200 smoother ordering). */
 int cf_setup_colour(int64_t n, const int64_t* indptr, const int64_t* indices,

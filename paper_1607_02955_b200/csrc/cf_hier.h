@@ -24,6 +24,10 @@ struct Plan {
     int64_t* send = nullptr;
     std::vector<int64_t> cseg;  // class c -> segments [cseg[c], cseg[c+1])
     std::vector<int64_t> cheavy;  // class c -> entries in its heavy rows
+    // distinct neighbour rows gathered by the heavy rows of: class c / the merged
+    // Jacobi classes / the whole plan (compulsory X reads of a k_seg launch)
+    std::vector<int64_t> cnbr;
+    int64_t merged_nbr = 0, all_nbr = 0;
     int32_t* seg_hv = nullptr;  // segment -> heavy index
     int32_t* h_row = nullptr;   // heavy index -> row
     int32_t* h_pos = nullptr;   // heavy index -> position in class order

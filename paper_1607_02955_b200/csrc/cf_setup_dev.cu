@@ -196,19 +196,24 @@ __global__ void __launch_bounds__(kT) k_urow_ptr(int64_t nc, int64_t U,
     urp[i] = lo;
 }
 
-// kept entries per row (+ 1 for the diagonal)
+// kept entries per row (+ 1 for the diagonal); one warp per row
 __global__ void __launch_bounds__(kT) k_row_counts(int64_t nc, const int64_t* __restrict__ urp,
                                                    const int32_t* __restrict__ keep,
                                                    int64_t* __restrict__ cnt) {
-    const int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x;
+    const int64_t i = ((int64_t)blockIdx.x * kT + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (i >= nc) return;
-    int64_t c = 1;
-    for (int64_t t = urp[i]; t < urp[i + 1]; ++t) c += keep[t];
-    cnt[i] = c;
+    int64_t c = 0;
+    for (int64_t t = urp[i] + lane; t < urp[i + 1]; t += 32) c += keep[t];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) cnt[i] = c + 1;
 }
 
-// write row i: kept off-diagonals in column order with the diagonal
-// (= minus their sum, accumulated in column order) at its sorted position
+// write row i (one warp per row): kept off-diagonals in column order with the
+// diagonal at its sorted position; diagonal = minus their sum, accumulated
+// per 32-entry chunk by a fixed shuffle tree and over the chunks in column
+// order (a fixed order for a given row)
 __global__ void __launch_bounds__(kT) k_emit_rows(int64_t nc, const int64_t* __restrict__ urp,
                                                   const uint64_t* __restrict__ ukey,
                                                   const double* __restrict__ sval,
@@ -216,23 +221,39 @@ __global__ void __launch_bounds__(kT) k_emit_rows(int64_t nc, const int64_t* __r
                                                   const int64_t* __restrict__ optr,
                                                   int64_t* __restrict__ oidx,
                                                   double* __restrict__ oval) {
-    const int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x;
+    const int64_t i = ((int64_t)blockIdx.x * kT + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (i >= nc) return;
-    int64_t o = optr[i];
-    int64_t dslot = -1;
+    const int64_t beg = urp[i], end = urp[i + 1];
+    const int64_t o0 = optr[i];
+    int64_t below = 0;  // kept entries left of the diagonal, found so far
+    int64_t done = 0;   // kept entries written so far
     double dg = 0.0;
-    for (int64_t t = urp[i]; t < urp[i + 1]; ++t) {
-        if (!keep[t]) continue;
-        const int64_t j = (int64_t)(ukey[t] % (uint64_t)nc);
-        if (dslot < 0 && j > i) dslot = o++;
-        oidx[o] = j;
-        oval[o] = sval[t];
-        ++o;
-        dg += -sval[t];
+    for (int64_t base = beg; base < end; base += 32) {
+        const int64_t t = base + lane;
+        const bool k = t < end && keep[t];
+        const int64_t j = k ? (int64_t)(ukey[t] % (uint64_t)nc) : 0;
+        const double v = k ? sval[t] : 0.0;
+        const unsigned m = __ballot_sync(0xffffffffu, k);
+        const unsigned lo = __ballot_sync(0xffffffffu, k && j < i);
+        if (k) {
+            const int r = __popc(m & ((1u << lane) - 1u));
+            // entries right of the diagonal shift by one slot
+            const int64_t slot = o0 + done + r + (j > i ? 1 : 0);
+            oidx[slot] = j;
+            oval[slot] = v;
+        }
+        double part = -v;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        dg += part;
+        done += __popc(m);
+        below += __popc(lo);
     }
-    if (dslot < 0) dslot = o++;
-    oidx[dslot] = i;
-    oval[dslot] = dg;
+    if (lane == 0) {
+        oidx[o0 + below] = i;
+        oval[o0 + below] = dg;
+    }
 }
 
 // result kept on the device between cf_coarse_*_dev and cf_coarse_fetch_dev
@@ -296,7 +317,7 @@ void finish_coarse(int device, int64_t nc, int64_t cnt, DBuf& key, DBuf& val) {
                                                sval.as<double>(), keep.as<int32_t>());
     k_urow_ptr<<<blocks_for(nc + 1), kT>>>(nc, U, ukey.as<uint64_t>(), urp.as<int64_t>());
     CF_CUDA(cudaMemset(rcnt.p, 0, sizeof(int64_t) * (nc + 1)));
-    k_row_counts<<<blocks_for(nc), kT>>>(nc, urp.as<int64_t>(), keep.as<int32_t>(), rcnt.as<int64_t>());
+    k_row_counts<<<blocks_for(nc * 32), kT>>>(nc, urp.as<int64_t>(), keep.as<int32_t>(), rcnt.as<int64_t>());
     c.optr.alloc(sizeof(int64_t) * (nc + 1));
     size_t sb = 0;
     CF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, sb, rcnt.as<int64_t>(), c.optr.as<int64_t>(), (int)(nc + 1)));
@@ -307,7 +328,7 @@ void finish_coarse(int device, int64_t nc, int64_t cnt, DBuf& key, DBuf& val) {
     c.nnz = total;
     c.oidx.alloc(sizeof(int64_t) * std::max<int64_t>(total, 1));
     c.oval.alloc(sizeof(double) * std::max<int64_t>(total, 1));
-    k_emit_rows<<<blocks_for(nc), kT>>>(nc, urp.as<int64_t>(), ukey.as<uint64_t>(), sval.as<double>(),
+    k_emit_rows<<<blocks_for(nc * 32), kT>>>(nc, urp.as<int64_t>(), ukey.as<uint64_t>(), sval.as<double>(),
                                         keep.as<int32_t>(), c.optr.as<int64_t>(), c.oidx.as<int64_t>(),
                                         c.oval.as<double>());
     CF_CUDA(cudaGetLastError());
@@ -318,6 +339,143 @@ void finish_coarse(int device, int64_t nc, int64_t cnt, DBuf& key, DBuf& val) {
 }  // namespace cf
 
 using namespace cf;
+
+// ---- Laplacian validation (solver.py:190-211) --------------------------------
+namespace cf {
+namespace {
+
+__device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
+    // non-negative doubles order like their bit patterns
+    atomicMax(reinterpret_cast<unsigned long long*>(addr), (unsigned long long)__double_as_longlong(v));
+}
+
+// out[0] = max |v|; out[1] = max |m - m^T|; out[3] = max off-diagonal value (if positive)
+__global__ void __launch_bounds__(kT) k_validate_entries(int64_t n, int64_t nnz,
+                                                         const int64_t* __restrict__ indptr,
+                                                         const int64_t* __restrict__ indices,
+                                                         const double* __restrict__ data,
+                                                         double* __restrict__ out) {
+    const int64_t p = (int64_t)blockIdx.x * kT + threadIdx.x;
+    if (p >= nnz) return;
+    const int64_t i = row_of(indptr, n, p);
+    const int64_t j = indices[p];
+    const double v = data[p];
+    atomic_max_nonneg(out + 0, fabs(v));
+    if (i != j) {
+        if (v > 0.0) atomic_max_nonneg(out + 3, v);
+        // mirror entry (j, i): rows are sorted
+        int64_t lo = indptr[j], hi = indptr[j + 1];
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (indices[mid] < i)
+                lo = mid + 1;
+            else
+                hi = mid;
+        }
+        const double t = (lo < indptr[j + 1] && indices[lo] == i) ? data[lo] : 0.0;
+        const double a = fabs(v - t);
+        if (a > 0.0) atomic_max_nonneg(out + 1, a);
+    }
+}
+// out[2] = max |row sum|
+__global__ void __launch_bounds__(kT) k_validate_rows(int64_t n, const int64_t* __restrict__ indptr,
+                                                      const double* __restrict__ data,
+                                                      double* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x;
+    if (i >= n) return;
+    double s = 0.0;
+    for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) s += data[p];
+    if (s != 0.0) atomic_max_nonneg(out + 2, fabs(s));
+}
+__global__ void __launch_bounds__(kT) k_cc_init32(int64_t n, int32_t* __restrict__ parent) {
+    const int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x;
+    if (i < n) parent[i] = (int32_t)i;
+}
+// hooking over the CSR entries (i < j once per undirected edge)
+__global__ void __launch_bounds__(kT) k_cc_hook_csr(int64_t n, int64_t nnz,
+                                                    const int64_t* __restrict__ indptr,
+                                                    const int64_t* __restrict__ indices,
+                                                    int32_t* __restrict__ parent,
+                                                    int* __restrict__ changed) {
+    const int64_t p = (int64_t)blockIdx.x * kT + threadIdx.x;
+    if (p >= nnz) return;
+    const int64_t j = indices[p];
+    const int64_t i = row_of(indptr, n, p);
+    if (i >= j) return;
+    const int32_t a = parent[i], b = parent[j];
+    if (a == b) return;
+    const int32_t hi = a > b ? a : b, lo = a > b ? b : a;
+    atomicMin(parent + hi, lo);
+    *changed = 1;
+}
+__global__ void __launch_bounds__(kT) k_cc_jump32(int64_t n, int32_t* __restrict__ parent) {
+    const int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x;
+    if (i >= n) return;
+    int32_t p = parent[i];
+    while (true) {
+        const int32_t q = parent[p];
+        if (q == p) break;
+        p = q;
+    }
+    parent[i] = p;
+}
+__global__ void __launch_bounds__(kT) k_count_roots(int64_t n, const int32_t* __restrict__ parent,
+                                                    unsigned long long* __restrict__ cnt) {
+    const int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x;
+    if (i < n && parent[i] == (int32_t)i) atomicAdd(cnt, 1ull);
+}
+
+}  // namespace
+}  // namespace cf
+
+// The checks of _validate_laplacian (solver.py:190-211) on GPU `device` for an
+// n x n CSR with sorted rows: out[0] = max |entry|, out[1] = max |m - m^T|,
+// out[2] = max |row sum|, out[3] = largest positive off-diagonal (0 if none);
+// *ncomp = connected components of the off-diagonal pattern.  Integer / max
+// reductions only: the verdict equals the host route's.
+extern "C" int cf_validate_laplacian_dev(int32_t device, int64_t n, const int64_t* indptr,
+                                         const int64_t* indices, const double* data,
+                                         double* out, int64_t* ncomp) {
+    CF_API_BEGIN
+    if (n < 0) throw cf::CfError(CF_DOMAIN, "negative size");
+    if ((uint64_t)n >= ((uint64_t)1 << 31)) throw cf::CfError(CF_RUNTIME, "too many nodes");
+    CF_CUDA(cudaSetDevice(device));
+    const int64_t nnz = n ? indptr[n] : 0;
+    cf::DBuf dp(sizeof(int64_t) * (n + 1)), di(sizeof(int64_t) * std::max<int64_t>(nnz, 1));
+    cf::DBuf dd(sizeof(double) * std::max<int64_t>(nnz, 1)), dout(sizeof(double) * 4);
+    cf::DBuf par(sizeof(int32_t) * std::max<int64_t>(n, 1)), chg(sizeof(int)), cnt(sizeof(unsigned long long));
+    if (n) CF_CUDA(cudaMemcpy(dp.p, indptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice));
+    if (nnz) {
+        CF_CUDA(cudaMemcpy(di.p, indices, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice));
+        CF_CUDA(cudaMemcpy(dd.p, data, sizeof(double) * nnz, cudaMemcpyHostToDevice));
+    }
+    CF_CUDA(cudaMemset(dout.p, 0, sizeof(double) * 4));
+    if (nnz)
+        cf::k_validate_entries<<<cf::blocks_for(nnz), cf::kT>>>(n, nnz, dp.as<int64_t>(),
+                                                                di.as<int64_t>(), dd.as<double>(),
+                                                                dout.as<double>());
+    if (n)
+        cf::k_validate_rows<<<cf::blocks_for(n), cf::kT>>>(n, dp.as<int64_t>(), dd.as<double>(),
+                                                           dout.as<double>());
+    if (n) cf::k_cc_init32<<<cf::blocks_for(n), cf::kT>>>(n, par.as<int32_t>());
+    for (int r = 0; nnz > 0 && r < 4096; ++r) {
+        CF_CUDA(cudaMemset(chg.p, 0, sizeof(int)));
+        cf::k_cc_hook_csr<<<cf::blocks_for(nnz), cf::kT>>>(n, nnz, dp.as<int64_t>(), di.as<int64_t>(),
+                                                          par.as<int32_t>(), chg.as<int>());
+        cf::k_cc_jump32<<<cf::blocks_for(n), cf::kT>>>(n, par.as<int32_t>());
+        int h = 0;
+        CF_CUDA(cudaMemcpy(&h, chg.p, sizeof(int), cudaMemcpyDeviceToHost));
+        if (!h) break;
+    }
+    CF_CUDA(cudaMemset(cnt.p, 0, sizeof(unsigned long long)));
+    if (n) cf::k_count_roots<<<cf::blocks_for(n), cf::kT>>>(n, par.as<int32_t>(), cnt.as<unsigned long long>());
+    CF_CUDA(cudaGetLastError());
+    unsigned long long c = 0;
+    CF_CUDA(cudaMemcpy(&c, cnt.p, sizeof(c), cudaMemcpyDeviceToHost));
+    CF_CUDA(cudaMemcpy(out, dout.p, sizeof(double) * 4, cudaMemcpyDeviceToHost));
+    *ncomp = (int64_t)c;
+    CF_API_END
+}
 
 // Coarse operator of one setup level on GPU `device`.  L: n x n CSR with its
 // diagonal stored, sorted rows.  map[i] = coarse index of fine node i (the

@@ -1140,11 +1140,15 @@ struct Ops {
     template <int MODE>
     static void seg(Hier& h, const Plan& pl, int64_t lo, int64_t hi, const int32_t* col,
                     const double* val, const int32_t* map, const double* div, const double* X,
-                    int level, bool sweep = false, double hnnz = -1.0, int jlim = 0x7fffffff) {
+                    int level, bool sweep = false, double hnnz = -1.0, int jlim = 0x7fffffff,
+                    int64_t nbr = -1) {
         if (hi <= lo) return;
         if (hnnz < 0)
             hnnz = (lo == 0 && hi == pl.nseg) ? (double)pl.heavy_nnz : (double)kSegNnz * (hi - lo);
-        ProfScope ps(h, "heavy_seg", level, 12.0 * hnnz + Vb(hi - lo) * 2, Vb(hnnz));
+        // compulsory bytes: matrix entries, one partial written (and read back by
+        // the row kernel) per segment, every distinct neighbour row of X once
+        if (nbr < 0) nbr = (lo == 0 && hi == pl.nseg && map == nullptr) ? pl.all_nbr : 0;
+        ProfScope ps(h, "heavy_seg", level, 12.0 * hnnz + Vb(hi - lo) * 2 + Vb(nbr), Vb(hnnz));
         const unsigned grid = (unsigned)((hi - lo + Lay<KC>::RPB - 1) / Lay<KC>::RPB);
         const int32_t* ord = sweep ? pl.sord_cls
                                    : (lo == 0 && hi == pl.nseg) ? pl.sord_all : nullptr;
@@ -1344,7 +1348,7 @@ struct Ops {
         const int pre = (l.pm.nheavy && s_hi - s_lo >= pre_seg_min()) ? 1 : 0;
         if (pre)
             seg<G_PLAIN>(h, l.pm, s_lo, s_hi, l.col, l.val, nullptr, nullptr, x, lev, true,
-                         (double)l.pm.cheavy[colr], jlim);
+                         (double)l.pm.cheavy[colr], jlim, 0);  // X rows: in the sweep's scope
         SegWork w = pre ? SegWork{} : segwork(h, l.pm, s_lo, s_hi);
         const int64_t hvy = pre ? l.pm.cheavy[colr] : 0;  // entries gathered by the k_seg launch
         const int64_t gnnz = from_zero ? 0 : first ? l.c_nnz_lo[colr] : l.c_nnz[colr] - hvy;
@@ -1378,7 +1382,7 @@ struct Ops {
         }
         if (pre)
             seg<G_PLAIN>(h, l.pm, s_lo, s_hi, l.col, l.val, nullptr, nullptr, x, lev, true,
-                         (double)hvy, jlim);
+                         (double)hvy, jlim, 0);  // X rows: in the sweep's scope (gnbr)
         SegWork w = pre ? SegWork{} : segwork(h, l.pm, s_lo, s_hi);
         const int64_t gnnz = first ? l.merged_nnz_lo : nnz - hvy;
         const int64_t gnbr = first ? l.merged_nbr_lo : l.merged_nbr;
@@ -2429,6 +2433,38 @@ static Plan build_plan(Hier& h, int64_t n, const int64_t* rp, const int32_t* ord
     }
     pl.cseg.push_back((int64_t)sb.size());
     pl.nseg = (int64_t)sb.size();
+    pl.cnbr.assign((size_t)ncls, 0);
+    if (pl.nheavy && col) {
+        // distinct neighbour rows per launch range (bytes model only)
+        const int K = std::min(ncls, std::max(0, merged_from));
+        std::vector<int32_t> stamp((size_t)n, -1);
+        std::vector<uint8_t> seen_m((size_t)n, 0), seen_a((size_t)n, 0);
+        int64_t hidx = 0;
+        for (int c = 0; c < ncls; ++c) {
+            int64_t lo = order ? cls_ptr[c] : 0, hi = order ? cls_ptr[c + 1] : n;
+            for (int64_t q = lo; q < hi; ++q) {
+                int64_t i = order ? order[q] : q;
+                if (rp[i + 1] - rp[i] <= kHeavyNnz) continue;
+                ++hidx;
+                for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+                    const int32_t j = col[p];
+                    if (stamp[(size_t)j] != c) {
+                        stamp[(size_t)j] = c;
+                        ++pl.cnbr[(size_t)c];
+                    }
+                    if (c >= K && !seen_m[(size_t)j]) {
+                        seen_m[(size_t)j] = 1;
+                        ++pl.merged_nbr;
+                    }
+                    if (!seen_a[(size_t)j]) {
+                        seen_a[(size_t)j] = 1;
+                        ++pl.all_nbr;
+                    }
+                }
+            }
+        }
+        (void)hidx;
+    }
     if (pl.nheavy) {
         pl.hv = upload(h, hv.data(), hv.size());
         pl.hsp = upload(h, hsp.data(), hsp.size());

@@ -521,6 +521,30 @@ def _validate_laplacian(matrix: sp.spmatrix) -> sp.csr_matrix:
         raise DomainError("matrix must be square")
     m = matrix.tocsr()
     n = m.shape[0]
+    if (m.nnz >= DEVICE_SETUP_MIN_NNZ and os.environ.get("CF_DEVICE_SETUP", "1") != "0"
+            and N.device_available()):
+        # large inputs: the same checks as max-reductions on the GPU
+        # (csrc/cf_setup_dev.cu); the transposes of the host route cost 14 s on C5
+        if not m.has_canonical_format:
+            m = m.copy()
+            m.sum_duplicates()  # sorted rows without repeated entries (the caller's matrix is untouched)
+        ip, ix = _csr64(m)
+        dv = np.ascontiguousarray(m.data, dtype=np.float64)
+        out = np.zeros(4)
+        ncomp = np.zeros(1, dtype=np.int64)
+        N.check(N.lib().cf_validate_laplacian_dev(_device_index(), n, N.ptr(ip, N.i64p),
+                                                  N.ptr(ix, N.i64p), N.ptr(dv, N.f64p),
+                                                  N.ptr(out, N.f64p), N.ptr(ncomp, N.i64p)))
+        tol = 1e-12 * n * max(float(out[0]), 1.0)
+        if out[1] > tol:
+            raise DomainError("matrix is not symmetric")
+        if out[2] > tol:
+            raise DomainError("row sums are not zero; not a Laplacian")
+        if out[3] > tol:
+            raise DomainError("positive off-diagonal entry; not a Laplacian")
+        if n > 1 and ncomp[0] > 1:
+            raise DomainError("Laplacian graph is not connected")
+        return _rebuild_laplacian(m)
     scale = float(np.abs(m.data).max()) if m.nnz else 0.0
     tol = 1e-12 * n * max(scale, 1.0)
     asym = abs(m - m.T)

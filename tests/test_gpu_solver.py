@@ -140,7 +140,7 @@ def test_block_widths_agree(rng):
     s = rng.standard_normal((200, g.n))
     s -= s.mean(axis=1, keepdims=True)
     full = np.stack([p.values for p in P.solve_many(h, s)])
-    for cnt in (1, 5, 9, 17, 33, 65, 129):
+    for cnt in (1, 5, 9, 17, 33, 65, 129, 161, 192):  # widths 1..128, 160, 192
         part = np.stack([p.values for p in P.solve_many(h, s[:cnt])])
         assert np.array_equal(part, full[:cnt]), cnt
 
@@ -417,3 +417,37 @@ def test_device_coarse_operators_match_host(rng):
     x = np.stack([p.values for p in P.solve_many(h_dev, b)])
     L = P.laplacian(g)
     assert max(np.linalg.norm(L @ x[i] - b[i]) / np.linalg.norm(b[i]) for i in range(4)) <= 1e-10
+
+
+def test_device_validation_matches_host(rng, monkeypatch):
+    """_validate_laplacian's checks (solver.py:190-211) on the GPU for large
+    inputs: same verdicts and the same rebuilt matrix as the host route."""
+    import scipy.sparse as sp
+    from paper_1607_02955_b200 import solver as S
+
+    u, v, w = random_connected_graph_edges(800, rng, weighted=True)
+    L = P.laplacian(P.Graph.from_edges(u, v, w, n=800))
+    host = S._validate_laplacian(L)
+    monkeypatch.setattr(S, "DEVICE_SETUP_MIN_NNZ", 1)
+    dev = S._validate_laplacian(L)
+    assert np.array_equal(host.indptr, dev.indptr) and np.array_equal(host.indices, dev.indices)
+    assert np.array_equal(host.data, dev.data)
+    bad = L.tolil(copy=True)
+    bad[3, 7] = bad[3, 7] - 0.5
+    with pytest.raises(P.DomainError, match="symmetric"):
+        S._validate_laplacian(bad.tocsr())
+    bad = L.tolil(copy=True)
+    bad[5, 5] = bad[5, 5] + 1.0
+    with pytest.raises(P.DomainError, match="row sums"):
+        S._validate_laplacian(bad.tocsr())
+    bad = L.tolil(copy=True)
+    j = L[9].indices[L[9].indices != 9][0]
+    bad[9, j] = 0.25
+    bad[j, 9] = 0.25
+    bad[9, 9] = bad[9, 9] - 0.25 + L[9, j]
+    bad[j, j] = bad[j, j] - 0.25 + L[j, 9]
+    with pytest.raises(P.DomainError, match="positive off-diagonal"):
+        S._validate_laplacian(bad.tocsr())
+    two = sp.block_diag([L, L], format="csr")
+    with pytest.raises(P.DomainError, match="not connected"):
+        S._validate_laplacian(two)
