@@ -237,6 +237,11 @@ int cf_csr_from_edges_dev(int32_t device, int64_t n, int64_t m, const int64_t* u
                           double* weights, int32_t* status);
 int cf_components_dev(int32_t device, int64_t n, int64_t m, const int64_t* eu, const int64_t* ev,
                       int64_t* root, int32_t* rounds);
+/* solver.py:264-275 relaxed_test_vectors' sweeps: x (n x count row-major) <-
+ * x + tril(L)^-1 (-(L x)), `sweeps` times; L sorted CSR with stored diagonal.
+ * Native replacement of the SuperLU triangular solves on hub graphs. */
+int cf_setup_relax(int64_t n, const int64_t* indptr, const int64_t* indices, const double* data,
+                   int32_t count, int32_t sweeps, double* x);
 /* Device-side coarse operators of the setup (
  * csrc/cf_setup_dev.cu).  L: n x n CSR with stored diagonal and sorted rows;
  * map[i] = coarse index of node i.  nf = 0: Galerkin product P^T L P of the

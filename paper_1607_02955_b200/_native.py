@@ -108,6 +108,7 @@ _SIGS = {
     "cf_coarse_operator_dev": (C.c_int, [C.c_int32, C.c_int64, i64p, i64p, f64p, i64p, C.c_int64,
                                          C.c_int64, i64p, i64p]),
     "cf_coarse_fetch_dev": (C.c_int, [i64p, i64p, f64p]),
+    "cf_setup_relax": (C.c_int, [C.c_int64, i64p, i64p, f64p, C.c_int32, C.c_int32, f64p]),
     "cf_validate_laplacian_dev": (C.c_int, [C.c_int32, C.c_int64, i64p, i64p, f64p, f64p, i64p]),
 }
 

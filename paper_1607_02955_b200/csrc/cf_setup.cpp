@@ -400,3 +400,64 @@ extern "C" int cf_setup_permute(int64_t nrows, const int64_t* indptr, const int6
     for (auto& x : th) x.join();
     return CF_OK;
 }
+
+// Test-vector relaxation (solver.py:264-275): `sweeps` forward Gauss-Seidel
+// sweeps on L x = 0 for the `count` columns of x (n x count, row-major),
+// x <- x + tril(L)^-1 (-(L x)) per sweep: residual with the old iterate, then
+// a forward substitution, all columns of a row together.  Used on hub graphs
+// (whose hierarchies are this build's own) in place of scipy's SuperLU
+// triangular solves; L has sorted rows with the diagonal stored.
+extern "C" int cf_setup_relax(int64_t n, const int64_t* indptr, const int64_t* indices,
+                              const double* data, int32_t count, int32_t sweeps, double* x) {
+    CF_API_BEGIN
+    if (count < 1 || count > 64) throw cf::CfError(CF_DOMAIN, "test vector count must be in [1, 64]");
+    const int k = count;
+    std::vector<double> r((size_t)n * k), y((size_t)n * k);
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const int64_t nt = std::min<int64_t>(hw, std::max<int64_t>(1, n / 4096));
+    const int64_t nnz = indptr[n];
+    std::vector<int64_t> cut(nt + 1, n);
+    cut[0] = 0;
+    for (int64_t t = 1; t < nt; ++t)
+        cut[t] = std::upper_bound(indptr, indptr + n + 1, nnz * t / nt) - indptr - 1;
+    for (int64_t t = 1; t <= nt; ++t) cut[t] = std::max(cut[t], cut[t - 1]);
+    for (int s = 0; s < sweeps; ++s) {
+        // r = -(L x), rows in parallel (each row: entries in column order)
+        std::vector<std::thread> th;
+        for (int64_t t = 0; t < nt; ++t)
+            th.emplace_back([&, t] {
+                double acc[64];
+                for (int64_t i = cut[t]; i < cut[t + 1]; ++i) {
+                    for (int c = 0; c < k; ++c) acc[c] = 0.0;
+                    for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) {
+                        const double a = data[p];
+                        const double* xj = x + (size_t)indices[p] * k;
+                        for (int c = 0; c < k; ++c) acc[c] += a * xj[c];
+                    }
+                    for (int c = 0; c < k; ++c) r[(size_t)i * k + c] = -acc[c];
+                }
+            });
+        for (auto& t : th) t.join();
+        // forward substitution tril(L) y = r (sequential over rows)
+        double acc[64];
+        for (int64_t i = 0; i < n; ++i) {
+            for (int c = 0; c < k; ++c) acc[c] = r[(size_t)i * k + c];
+            double d = 0.0;
+            for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) {
+                const int64_t j = indices[p];
+                if (j > i) break;
+                if (j == i) {
+                    d = data[p];
+                    break;
+                }
+                const double a = data[p];
+                const double* yj = y.data() + (size_t)j * k;
+                for (int c = 0; c < k; ++c) acc[c] -= a * yj[c];
+            }
+            if (d == 0.0) throw cf::CfError(CF_DOMAIN, "zero diagonal in the test-vector relaxation");
+            for (int c = 0; c < k; ++c) y[(size_t)i * k + c] = acc[c] / d;
+        }
+        for (size_t q = 0; q < (size_t)n * k; ++q) x[q] += y[q];
+    }
+    CF_API_END
+}

@@ -608,6 +608,7 @@ def _elim_select(matrix: sp.csr_matrix, cap: int) -> np.ndarray:
 # everywhere else the host route keeps hierarchies bit-identical to the
 # reference's goldens (C1-C3).  The device sums equal keys in sorted order, scipy in
 # its SpGEMM order: values agree to rounding (tests/test_gpu_solver.py).
+_native_relax_on = False  # set per setup() call: hub graphs only
 DEVICE_SETUP_MIN_NNZ = 1 << 21
 DEVICE_SETUP_MIN_N0 = STALL_BREAKER_MIN_N0
 _device_setup_on = False
@@ -670,6 +671,18 @@ def relaxed_test_vectors(matrix: sp.csr_matrix, count: int, rng: np.random.Gener
     (solver.py:264-275); same RNG draws and sweeps as the reference."""
     x = rng.standard_normal((matrix.shape[0], count))
     x -= x.mean(axis=0, keepdims=True)
+    if _native_relax_on and matrix.has_sorted_indices and count <= 64:
+        # hub graphs (hierarchies are this build's own): the same sweeps as a
+        # native loop (csrc/cf_setup.cpp) instead of SuperLU triangular solves
+        # (16 of the 36 s of the C5 host setup)
+        ip, ix = _csr64(matrix)
+        dv = np.ascontiguousarray(matrix.data, dtype=np.float64)
+        x = np.ascontiguousarray(x)
+        N.check(N.lib().cf_setup_relax(matrix.shape[0], N.ptr(ip, N.i64p), N.ptr(ix, N.i64p),
+                                       N.ptr(dv, N.f64p), count, TEST_VECTOR_SWEEPS,
+                                       N.ptr(x, N.f64p)))
+        x -= x.mean(axis=0, keepdims=True)
+        return x
     low = sp.tril(matrix, 0, format="csr")
     for _ in range(TEST_VECTOR_SWEEPS):
         x += spsolve_triangular(low, -(matrix @ x), lower=True)
@@ -778,8 +791,9 @@ def setup(matrix: sp.spmatrix, config: SolverConfig | None = None,
     """
     config = config or SolverConfig()
     current = _validate_laplacian(matrix)
-    global _device_setup_on
+    global _device_setup_on, _native_relax_on
     _device_setup_on = False
+    _native_relax_on = False
     rng = np.random.default_rng(config.seed)
     levels: list[Level] = []
     preferred = LevelKind.ELIMINATION
@@ -801,6 +815,7 @@ def setup(matrix: sp.spmatrix, config: SolverConfig | None = None,
     if stall_breaker is not False and n0 > DEVICE_SETUP_MIN_N0:
         od0 = np.diff(current.indptr) - 1
         _device_setup_on = bool(od0.max() > HUB_DEGREE_RATIO * max(od0.mean(), 1.0))
+        _native_relax_on = _device_setup_on and os.environ.get("CF_NATIVE_RELAX", "1") != "0"
     while current.shape[0] > config.max_direct_size:
         n_cur = current.shape[0]
         need = MIN_REDUCTION * n_cur

@@ -266,3 +266,29 @@ def test_hub_level_rule():
     h1 = P.setup(lap)
     h2 = P.setup(lap, stall_breaker=False)
     assert h1.level_sizes == h2.level_sizes
+
+
+def test_native_relaxation_matches_scipy_sweeps(rng):
+    """cf_setup_relax (hub graphs' test-vector relaxation) performs the sweeps of
+    solver.py:264-275: x += tril(L)^-1 (-(L x)), three times."""
+    import scipy.sparse as sp
+    from scipy.sparse.linalg import spsolve_triangular
+    from paper_1607_02955_b200 import solver as S
+
+    u, v, w = random_connected_graph_edges(500, rng, weighted=True)
+    L = S._validate_laplacian(P.laplacian(P.Graph.from_edges(u, v, w, n=500)))
+    seed = 5
+    ref = S.relaxed_test_vectors(L, 4, np.random.default_rng(seed))
+    S._native_relax_on = True
+    try:
+        got = S.relaxed_test_vectors(L, 4, np.random.default_rng(seed))
+    finally:
+        S._native_relax_on = False
+    assert np.allclose(got, ref, rtol=1e-11, atol=1e-13)
+    x = np.random.default_rng(seed).standard_normal((500, 4))
+    x -= x.mean(axis=0, keepdims=True)
+    low = sp.tril(L, 0, format="csr")
+    for _ in range(3):
+        x += spsolve_triangular(low, -(L @ x), lower=True)
+    x -= x.mean(axis=0, keepdims=True)
+    assert np.allclose(got, x, rtol=1e-11, atol=1e-13)
