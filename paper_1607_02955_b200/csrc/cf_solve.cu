@@ -25,6 +25,9 @@
 #include "cf_kernels.cuh"
 #include "cfcent_b200.h"
 
+#ifndef CF_HOIST_OWN
+#define CF_HOIST_OWN 0  // experiment knob: own-row loads before the gather (measured below)
+#endif
 #ifndef CF_RED_CTAS
 #define CF_RED_CTAS 3  // min CTAs/SM for the reduction / restriction gather kernels
 #endif
@@ -78,12 +81,23 @@ __global__ void __launch_bounds__(kThreads, (KC > 128 ? 2 : CF_RED_CTAS)) k_resi
         zero(acc);
         zero(x);
         double d = 0.0;
+#if CF_HOIST_OWN
+        // the row's own B / X / diagonal loads are issued before the gather so
+        // they overlap its latency chain (indices -> neighbour rows)
+        DV<V> b = ldv<V>(B + i * KC + c0);
+        if (!x_zero) {
+            x = ldv<V>(X + i * KC + c0);
+            d = diag[i];
+            row_sum<KC, G_PLAIN>(H, i, col, val, rp[i], rp[i + 1], nullptr, nullptr, X, c0, acc);
+        }
+#else
         if (!x_zero) {
             row_sum<KC, G_PLAIN>(H, i, col, val, rp[i], rp[i + 1], nullptr, nullptr, X, c0, acc);
             x = ldv<V>(X + i * KC + c0);
             d = diag[i];
         }
         DV<V> b = ldv<V>(B + i * KC + c0);
+#endif
         DV<V> out;
 #pragma unroll
         for (int t = 0; t < V; ++t) {
@@ -649,9 +663,15 @@ __global__ void __launch_bounds__(kThreads, (KC > 128 ? 2 : CF_RED_CTAS)) k_agg_
         int64_t i = amem[q];
         DV<V> acc;
         zero(acc);
+#if CF_HOIST_OWN
+        DV<V> b = ldv<V>(B + i * KC + c0), x = ldv<V>(X + i * KC + c0);
+        double d = diag[i];
+        row_sum<KC, G_PLAIN>(H, i, col, val, rp[i], rp[i + 1], nullptr, nullptr, X, c0, acc);
+#else
         row_sum<KC, G_PLAIN>(H, i, col, val, rp[i], rp[i + 1], nullptr, nullptr, X, c0, acc);
         DV<V> b = ldv<V>(B + i * KC + c0), x = ldv<V>(X + i * KC + c0);
         double d = diag[i];
+#endif
 #pragma unroll
         for (int t = 0; t < V; ++t) out.v[t] += b.v[t] - fma(d, x.v[t], acc.v[t]);
     }
@@ -705,9 +725,15 @@ __global__ void __launch_bounds__(kThreads, (KC > 128 ? 2 : CF_RED_CTAS)) k_agg_
             if (i >= n || !lane_ok) break;
             DV<V> acc;
             zero(acc);
+#if CF_HOIST_OWN
+            DV<V> d = ldv<V>(Xc + (size_t)(agg ? agg[i] : i) * KC + c0);
+            double dg = diag[i];
+            row_sum<KC, G_PLAIN>(H, i, col, val, rp[i], rp[i + 1], nullptr, nullptr, Xc, c0, acc);
+#else
             row_sum<KC, G_PLAIN>(H, i, col, val, rp[i], rp[i + 1], nullptr, nullptr, Xc, c0, acc);
             DV<V> d = ldv<V>(Xc + (size_t)(agg ? agg[i] : i) * KC + c0);
             double dg = diag[i];
+#endif
 #pragma unroll
             for (int t = 0; t < V; ++t) {
                 double ld = fma(dg, d.v[t], acc.v[t]);
