@@ -74,7 +74,12 @@ constexpr int kGatherCtas = CF_GATHER_CTAS;  // min CTAs per SM for sweep kernel
 // only the first KC lanes work (narrow blocks are latency-bound anyway).
 template <int KC>
 struct Lay {
-    static constexpr int LPR = KC < 32 ? KC : 32;  // working lanes per row group
+    // working lanes per row group.  Widths 160 / 192 (remainder chunks) keep 32
+    // lanes of 5 / 6 columns (64 / 128-bit accesses).  The alternative of 20 /
+    // 24 lanes of 8 columns (two 256-bit accesses per lane) was measured slower
+    // on C5 (block solve 818 vs 690 ms at 160, 844 vs 795 ms at 192): fewer
+    // index entries per chunk and fewer neighbour rows in flight per warp.
+    static constexpr int LPR = KC < 32 ? KC : 32;
     static constexpr int VEC = KC / LPR;           // doubles per lane
     static constexpr int RPW = 1;                  // row groups per warp
     static constexpr int RPB = kWarps;             // row groups per CTA pass
@@ -281,9 +286,11 @@ __device__ __forceinline__ void gather_row_from(const int32_t* __restrict__ col,
             double a[G], d[G];
 #pragma unroll
             for (int u = 0; u < G; ++u) {
-                int j = __shfl_sync(MASK, jj, u0 + u, W);
-                a[u] = __shfl_sync(MASK, aa, u0 + u, W);
-                if constexpr (MODE == G_ELIM || MODE == G_DIV) d[u] = __shfl_sync(MASK, dd, u0 + u, W);
+                // source lanes are absolute (< W), so the full shuffle width also
+                // serves row groups whose lane count is not a power of two
+                int j = __shfl_sync(MASK, jj, u0 + u, 32);
+                a[u] = __shfl_sync(MASK, aa, u0 + u, 32);
+                if constexpr (MODE == G_ELIM || MODE == G_DIV) d[u] = __shfl_sync(MASK, dd, u0 + u, 32);
                 if (u0 + u < cnt && j < jlim)
                     x[u] = ldv<V>(X + (size_t)j * KC + c0);
                 else

@@ -26,7 +26,11 @@
 #include "cfcent_b200.h"
 
 #ifndef CF_HOIST_OWN
-#define CF_HOIST_OWN 0  // experiment knob: own-row loads before the gather (measured below)
+// experiment knob: the row's own B / X / diagonal loads before the gather in the
+// residual / restriction / line-search kernels.  Measured on C5: 1,612 vs
+// 1,584 ms per step (more registers live across the gather, 128 -> 240 bytes
+// of spills in k_residual<128>), so it stays off.
+#define CF_HOIST_OWN 0
 #endif
 #ifndef CF_RED_CTAS
 #define CF_RED_CTAS 3  // min CTAs/SM for the reduction / restriction gather kernels
@@ -2393,6 +2397,11 @@ static T* upload(Hier& h, const T* src, size_t cnt);
 // entries, and all segments of a launch are processed window by window: the
 // warps in flight then gather from one window of X (win_rows x 8 KC bytes,
 // 32 MB at KC = 128) that stays in the L2 while every hub row consumes it.
+// Measured on C5 (ms per JL estimate, profiles/r02/window_sweep_c5.txt):
+// windows off ~1,780; 32,768 rows with degree threshold 128 / 256 / 1,024:
+// 1,661 / 1,584 / 1,527 (a lower threshold cuts medium rows into many short
+// segments, each with a partial to write and read back; 2,048-16,384 are no
+// better than 1,024); 16,384 / 65,536 rows at threshold 256: 1,673 / 1,560.
 static int64_t win_rows() {
     static const int64_t w = [] {
         const char* e = std::getenv("CF_WIN_ROWS");
@@ -2403,7 +2412,7 @@ static int64_t win_rows() {
 static int64_t win_deg() {
     static const int64_t d = [] {
         const char* e = std::getenv("CF_WIN_DEG");
-        return e ? (int64_t)std::atoll(e) : (int64_t)256;
+        return e ? (int64_t)std::atoll(e) : (int64_t)1024;
     }();
     return d;
 }
