@@ -40,6 +40,12 @@ struct Plan {
     // sord_all: sorted over the whole plan (k_seg launches).  nullptr: id order.
     int32_t* sord_cls = nullptr;
     int32_t* sord_all = nullptr;
+    // bounded first sweeps (x = 0 above the class's first row): per heavy row
+    // the leading segments with a column below that bound (hlo), and their
+    // window-sorted order per launch range (sord_lo, ranges cseg_lo)
+    int32_t* hlo = nullptr;
+    int32_t* sord_lo = nullptr;
+    std::vector<int64_t> cseg_lo;  // launch range r -> [cseg_lo[r], cseg_lo[r+1]) in sord_lo
     int64_t nwin_seg = 0;       // segments cut at column-window boundaries
 };
 
@@ -80,6 +86,10 @@ struct DLevel {
     std::vector<int64_t> c_rows, c_nnz, c_nbr, c_nnz_lo, c_nbr_lo;
     int64_t merged_nbr = 0;  // distinct neighbour rows of the merged Jacobi classes
     int64_t merged_nbr_lo = 0, merged_nnz_lo = 0;
+    // the same counts over the light rows only (<= kHeavyNnz entries): what a
+    // sweep kernel gathers itself when the heavy rows' segments run in k_seg
+    std::vector<int64_t> c_nbr_light;
+    int64_t merged_nbr_light = 0;
     int64_t w_nnz = 0;  // elimination: nnz(W_cf)
     int gs_classes = 0;  // colour classes swept one by one (<= kGsClasses)
     bool merged = false; // classes >= kGsClasses merged into one Jacobi step

@@ -393,6 +393,10 @@ struct HeavyDev {
     const int32_t* hv = nullptr;   // row -> heavy index or -1
     const int64_t* hsp = nullptr;  // heavy index -> first segment (size nheavy+1)
     const double* P = nullptr;     // segment partials, [nseg][KC]
+    // heavy index -> number of leading segments that hold a column below the
+    // row's first-sweep bound (the start of its class range); the bounded
+    // first sweep of a cycle computes and sums only those
+    const int32_t* hlo = nullptr;
 };
 
 // In-kernel heavy rows for the smoother sweeps: the launch carries extra warps,
@@ -449,14 +453,14 @@ __device__ __forceinline__ bool seg_item(const SegWork& w, int64_t s,
 // acc += the segment partials of heavy row hv, in segment order
 template <int KC>
 __device__ __forceinline__ void heavy_partials(const HeavyDev& H, int hv, int c0,
-                                               DV<Lay<KC>::VEC>& acc) {
+                                               DV<Lay<KC>::VEC>& acc, bool lo_only = false) {
     constexpr int V = Lay<KC>::VEC;
     // a hub row has thousands of partials and one warp sums them: keep NB
     // loads in flight (same register budget as the gather loop); the adds stay
     // in segment order
     constexpr int NB0 = CF_GATHER_DOUBLES / V > 0 ? CF_GATHER_DOUBLES / V : 1;
     constexpr int NB = NB0 > 8 ? 8 : NB0;
-    const int64_t s0 = H.hsp[hv], s1 = H.hsp[hv + 1];
+    const int64_t s0 = H.hsp[hv], s1 = lo_only ? s0 + H.hlo[hv] : H.hsp[hv + 1];
     int64_t sgi = s0;
     for (; sgi + NB <= s1; sgi += NB) {
         DV<V> q[NB];

@@ -356,25 +356,38 @@ __global__ void __launch_bounds__(kT) k_validate_entries(int64_t n, int64_t nnz,
                                                          const double* __restrict__ data,
                                                          double* __restrict__ out) {
     const int64_t p = (int64_t)blockIdx.x * kT + threadIdx.x;
-    if (p >= nnz) return;
-    const int64_t i = row_of(indptr, n, p);
-    const int64_t j = indices[p];
-    const double v = data[p];
-    atomic_max_nonneg(out + 0, fabs(v));
-    if (i != j) {
-        if (v > 0.0) atomic_max_nonneg(out + 3, v);
-        // mirror entry (j, i): rows are sorted
-        int64_t lo = indptr[j], hi = indptr[j + 1];
-        while (lo < hi) {
-            const int64_t mid = (lo + hi) >> 1;
-            if (indices[mid] < i)
-                lo = mid + 1;
-            else
-                hi = mid;
+    double m_abs = 0.0, m_asym = 0.0, m_pos = 0.0;
+    if (p < nnz) {
+        const int64_t i = row_of(indptr, n, p);
+        const int64_t j = indices[p];
+        const double v = data[p];
+        m_abs = fabs(v);
+        if (i != j) {
+            if (v > 0.0) m_pos = v;
+            // mirror entry (j, i): rows are sorted
+            int64_t lo = indptr[j], hi = indptr[j + 1];
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (indices[mid] < i)
+                    lo = mid + 1;
+                else
+                    hi = mid;
+            }
+            const double t = (lo < indptr[j + 1] && indices[lo] == i) ? data[lo] : 0.0;
+            m_asym = fabs(v - t);
         }
-        const double t = (lo < indptr[j + 1] && indices[lo] == i) ? data[lo] : 0.0;
-        const double a = fabs(v - t);
-        if (a > 0.0) atomic_max_nonneg(out + 1, a);
+    }
+    // one atomic per warp and quantity (max is order-independent)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        m_abs = fmax(m_abs, __shfl_xor_sync(0xffffffffu, m_abs, o));
+        m_asym = fmax(m_asym, __shfl_xor_sync(0xffffffffu, m_asym, o));
+        m_pos = fmax(m_pos, __shfl_xor_sync(0xffffffffu, m_pos, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (m_abs > 0.0) atomic_max_nonneg(out + 0, m_abs);
+        if (m_asym > 0.0) atomic_max_nonneg(out + 1, m_asym);
+        if (m_pos > 0.0) atomic_max_nonneg(out + 3, m_pos);
     }
 }
 // out[2] = max |row sum|

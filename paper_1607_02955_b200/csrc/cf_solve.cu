@@ -502,7 +502,7 @@ __global__ void __launch_bounds__(kThreads, SHORT ? 2 : (KC > 128 ? 2 : kGatherC
                     const double d = diag[r];
                     zero(acc);
                     if (heavy)
-                        heavy_partials<KC>(H, H.hv[r], c0, acc);
+                        heavy_partials<KC>(H, H.hv[r], c0, acc, pre == 2);
                     else
                         gather_row_from<KC, G_PLAIN>(col, val, beg, end, nullptr, nullptr, X, c0,
                                                      acc, jj, aa, dd, jlim);
@@ -525,7 +525,7 @@ __global__ void __launch_bounds__(kThreads, SHORT ? 2 : (KC > 128 ? 2 : kGatherC
             DV<V> b = ldv<V>(B + i * KC + c0);
             const double d = diag[i];
             if (heavy)
-                heavy_partials<KC>(H, H.hv[i], c0, acc);
+                heavy_partials<KC>(H, H.hv[i], c0, acc, pre == 2);
             else
                 gather_row<KC, G_PLAIN>(col, val, beg, end, nullptr, nullptr, X, c0, acc, jlim);
 #pragma unroll
@@ -579,7 +579,7 @@ __global__ void __launch_bounds__(kThreads, SHORT ? 2 : (KC > 128 ? 2 : kGatherC
                     const double d = diag[r];
                     zero(acc);
                     if (heavy)
-                        heavy_partials<KC>(H, H.hv[r], c0, acc);
+                        heavy_partials<KC>(H, H.hv[r], c0, acc, pre == 2);
                     else
                         gather_row_from<KC, G_PLAIN>(col, val, beg, end, nullptr, nullptr, X, c0,
                                                      acc, jj, aa, dd, jlim);
@@ -602,7 +602,7 @@ __global__ void __launch_bounds__(kThreads, SHORT ? 2 : (KC > 128 ? 2 : kGatherC
         DV<V> b = ldv<V>(B + i * KC + c0);
         const double d = diag[i];
         if (heavy)
-            heavy_partials<KC>(H, H.hv[i], c0, acc);
+            heavy_partials<KC>(H, H.hv[i], c0, acc, pre == 2);
         else
             gather_row<KC, G_PLAIN>(col, val, beg, end, nullptr, nullptr, X, c0, acc, jlim);
 #pragma unroll
@@ -1144,6 +1144,7 @@ struct Ops {
             d.hv = pl.hv;
             d.hsp = pl.hsp;
             d.P = h.SP;
+            d.hlo = pl.hlo;
         }
         return d;
     }
@@ -1171,7 +1172,22 @@ struct Ops {
     static void seg(Hier& h, const Plan& pl, int64_t lo, int64_t hi, const int32_t* col,
                     const double* val, const int32_t* map, const double* div, const double* X,
                     int level, bool sweep = false, double hnnz = -1.0, int jlim = 0x7fffffff,
-                    int64_t nbr = -1) {
+                    int64_t nbr = -1, int lo_range = -1) {
+        if (lo_range >= 0) {
+            // bounded first sweep: only the segments that hold a column below the
+            // bound (listed per launch range in sord_lo)
+            const int64_t a = pl.cseg_lo[(size_t)lo_range], b = pl.cseg_lo[(size_t)lo_range + 1];
+            if (b <= a) return;
+            ProfScope ps(h, "heavy_seg", level, 12.0 * hnnz + Vb(b - a) * 2, Vb(hnnz));
+            const unsigned grid = (unsigned)((b - a + Lay<KC>::RPB - 1) / Lay<KC>::RPB);
+            if (grid <= kDeepSegCtas)
+                launch_k(k_seg<KC, MODE, true>, dim3(grid), dim3(kThreads), 0, h.s, a, b, pl.sbeg,
+                         pl.send, col, val, map, div, X, h.SP, (const int32_t*)pl.sord_lo, jlim);
+            else
+                launch_k(k_seg<KC, MODE, false>, dim3(grid), dim3(kThreads), 0, h.s, a, b, pl.sbeg,
+                         pl.send, col, val, map, div, X, h.SP, (const int32_t*)pl.sord_lo, jlim);
+            return;
+        }
         if (hi <= lo) return;
         if (hnnz < 0)
             hnnz = (lo == 0 && hi == pl.nseg) ? (double)pl.heavy_nnz : (double)kSegNnz * (hi - lo);
@@ -1375,14 +1391,21 @@ struct Ops {
         const int lev = (int)(&l - &h.L[0]);
         const int64_t s_lo = from_zero ? 0 : l.pm.cseg[colr], s_hi = from_zero ? 0 : l.pm.cseg[colr + 1];
         const int jlim = first ? beg : 0x7fffffff;
-        const int pre = (l.pm.nheavy && s_hi - s_lo >= pre_seg_min()) ? 1 : 0;
-        if (pre)
+        int pre = (l.pm.nheavy && s_hi - s_lo >= pre_seg_min()) ? 1 : 0;
+        if (pre && first && l.pm.hlo) {
+            pre = 2;  // bounded: only the segments with a column below the bound
             seg<G_PLAIN>(h, l.pm, s_lo, s_hi, l.col, l.val, nullptr, nullptr, x, lev, true,
-                         (double)l.pm.cheavy[colr], jlim, 0);  // X rows: in the sweep's scope
+                         (double)std::min(l.pm.cheavy[colr], l.c_nnz_lo[colr]), jlim, 0, colr);
+        } else if (pre)
+            seg<G_PLAIN>(h, l.pm, s_lo, s_hi, l.col, l.val, nullptr, nullptr, x, lev, true,
+                         (double)l.pm.cheavy[colr], jlim, first ? 0 : l.pm.cnbr[colr]);
         SegWork w = pre ? SegWork{} : segwork(h, l.pm, s_lo, s_hi);
         const int64_t hvy = pre ? l.pm.cheavy[colr] : 0;  // entries gathered by the k_seg launch
         const int64_t gnnz = from_zero ? 0 : first ? l.c_nnz_lo[colr] : l.c_nnz[colr] - hvy;
-        const int64_t gnbr = from_zero ? 0 : first ? l.c_nbr_lo[colr] : l.c_nbr[colr];
+        // with the segments in their own launch the sweep kernel gathers for its
+        // light rows only (the k_seg scope counts the heavy rows' neighbour rows)
+        const int64_t gnbr = from_zero ? 0 : first ? l.c_nbr_lo[colr]
+                                           : pre ? l.c_nbr_light[colr] : l.c_nbr[colr];
         ProfScope ps(h, "gs_sweep", lev,
                      12.0 * (l.c_nnz[colr] - hvy) + 20.0 * cnt + Vb(2 * cnt + gnbr), Vb(gnnz));
         const int rpw = short_rpw(cnt, l.c_nnz[colr]);
@@ -1404,18 +1427,22 @@ struct Ops {
         const int lev = (int)(&l - &h.L[0]);
         const int64_t s_lo = l.pm.cseg[K], s_hi = l.pm.cseg[l.ncolors];
         const int jlim = first ? beg : 0x7fffffff;
-        const int pre = (l.pm.nheavy && s_hi - s_lo >= pre_seg_min()) ? 1 : 0;
+        int pre = (l.pm.nheavy && s_hi - s_lo >= pre_seg_min()) ? 1 : 0;
         int64_t nnz = 0, hvy = 0;
         for (int c = K; c < l.ncolors; ++c) {
             nnz += l.c_nnz[c];
             if (pre) hvy += l.pm.cheavy[c];
         }
-        if (pre)
+        if (pre && first && l.pm.hlo) {
+            pre = 2;  // bounded: only the segments with a column below the bound
             seg<G_PLAIN>(h, l.pm, s_lo, s_hi, l.col, l.val, nullptr, nullptr, x, lev, true,
-                         (double)hvy, jlim, 0);  // X rows: in the sweep's scope (gnbr)
+                         (double)std::min(hvy, l.merged_nnz_lo), jlim, 0, K);
+        } else if (pre)
+            seg<G_PLAIN>(h, l.pm, s_lo, s_hi, l.col, l.val, nullptr, nullptr, x, lev, true,
+                         (double)hvy, jlim, first ? 0 : l.pm.merged_nbr);
         SegWork w = pre ? SegWork{} : segwork(h, l.pm, s_lo, s_hi);
         const int64_t gnnz = first ? l.merged_nnz_lo : nnz - hvy;
-        const int64_t gnbr = first ? l.merged_nbr_lo : l.merged_nbr;
+        const int64_t gnbr = first ? l.merged_nbr_lo : pre ? l.merged_nbr_light : l.merged_nbr;
         {
             ProfScope ps(h, "jacobi_merged", lev,
                          12.0 * (nnz - hvy) + 20.0 * cnt + Vb(2 * cnt + gnbr), Vb(gnnz));
@@ -2510,6 +2537,42 @@ static Plan build_plan(Hier& h, int64_t n, const int64_t* rp, const int32_t* ord
         pl.h_pos = upload(h, hpos.data(), hpos.size());
         pl.cntr = (int*)h.dalloc(sizeof(int) * pl.nheavy);
         CF_CUDA(cudaMemset(pl.cntr, 0, sizeof(int) * pl.nheavy));
+        if (col && order) {
+            // leading segments below the first-sweep bound of the row's class
+            const int K = std::min(ncls, std::max(0, merged_from));
+            std::vector<int32_t> hlo((size_t)pl.nheavy, 0), lo_list;
+            std::vector<int32_t> key_lo;
+            pl.cseg_lo.assign(1, 0);
+            auto range_of = [&](int c) { return c < K ? c : K; };
+            int cur = 0;
+            for (int c = 0; c < ncls; ++c) {
+                const int r = range_of(c);
+                while (cur < r) {
+                    pl.cseg_lo.push_back((int64_t)lo_list.size());
+                    ++cur;
+                }
+                const int64_t bound = cls_ptr[r];
+                for (int64_t sgi = pl.cseg[c]; sgi < pl.cseg[c + 1]; ++sgi)
+                    if (col[sb[(size_t)sgi]] < bound) {
+                        ++hlo[(size_t)shv[(size_t)sgi]];
+                        lo_list.push_back((int32_t)sgi);
+                        key_lo.push_back(W > 0 ? (int32_t)(col[sb[(size_t)sgi]] / W) : 0);
+                    }
+            }
+            while ((int)pl.cseg_lo.size() < std::min(ncls, K + 1) + 1)
+                pl.cseg_lo.push_back((int64_t)lo_list.size());
+            pl.cseg_lo.back() = (int64_t)lo_list.size();
+            // window order inside every launch range
+            std::vector<int32_t> idx(lo_list.size());
+            for (size_t t = 0; t < idx.size(); ++t) idx[t] = (int32_t)t;
+            for (size_t r = 0; r + 1 < pl.cseg_lo.size(); ++r)
+                std::stable_sort(idx.begin() + pl.cseg_lo[r], idx.begin() + pl.cseg_lo[r + 1],
+                                 [&](int32_t x, int32_t y) { return key_lo[(size_t)x] < key_lo[(size_t)y]; });
+            std::vector<int32_t> sorted(lo_list.size());
+            for (size_t t = 0; t < idx.size(); ++t) sorted[t] = lo_list[(size_t)idx[t]];
+            pl.hlo = upload(h, hlo.data(), hlo.size());
+            if (!sorted.empty()) pl.sord_lo = upload(h, sorted.data(), sorted.size());
+        }
         if (windows) {
             // processing orders: stable sort by the window of the first entry
             std::vector<int32_t> key((size_t)pl.nseg), ord((size_t)pl.nseg);
@@ -2650,12 +2713,13 @@ extern "C" int cf_hier_create(int32_t nlev, const CfLevelDesc* ds, int32_t devic
                 // colour-class sizes for the algorithmic-bytes model
                 // (_lo: entries / distinct rows with j below the class's first
                 // row, what the bounded first sweep reads on a contiguous level)
-                std::vector<int64_t> stamp(d.n, -1);
+                std::vector<int64_t> stamp(d.n, -1), stamp_l(d.n, -1);
                 for (int c = 0; c < d.n_colors; ++c) {
                     int64_t rows = d.color_ptr[c + 1] - d.color_ptr[c], nnz = 0, nbr = 0;
-                    int64_t nnz_lo = 0, nbr_lo = 0;
+                    int64_t nnz_lo = 0, nbr_lo = 0, nbr_light = 0;
                     for (int32_t q = d.color_ptr[c]; q < d.color_ptr[c + 1]; ++q) {
                         int32_t i = d.color_rows[q];
+                        const bool light = d.rowptr[i + 1] - d.rowptr[i] <= kHeavyNnz;
                         for (int64_t p = d.rowptr[i]; p < d.rowptr[i + 1]; ++p) {
                             ++nnz;
                             int32_t jn = d.col[p];
@@ -2666,8 +2730,13 @@ extern "C" int cf_hier_create(int32_t nlev, const CfLevelDesc* ds, int32_t devic
                                 ++nbr;
                                 nbr_lo += lo;
                             }
+                            if (light && stamp_l[jn] != c) {
+                                stamp_l[jn] = c;
+                                ++nbr_light;
+                            }
                         }
                     }
+                    l.c_nbr_light.push_back(nbr_light);
                     l.c_rows.push_back(rows);
                     l.c_nnz.push_back(nnz);
                     l.c_nbr.push_back(nbr);
@@ -2676,16 +2745,21 @@ extern "C" int cf_hier_create(int32_t nlev, const CfLevelDesc* ds, int32_t devic
                 }
                 // distinct neighbour rows of the merged (Jacobi) classes, counted once
                 if (l.merged) {
-                    std::vector<uint8_t> seen(d.n, 0);
+                    std::vector<uint8_t> seen(d.n, 0), seen_l(d.n, 0);
                     const int32_t mbeg = d.color_ptr[l.gs_classes];
                     for (int32_t q = mbeg; q < d.color_ptr[d.n_colors]; ++q) {
                         int32_t i = d.color_rows[q];
+                        const bool light = d.rowptr[i + 1] - d.rowptr[i] <= kHeavyNnz;
                         for (int64_t p = d.rowptr[i]; p < d.rowptr[i + 1]; ++p) {
                             l.merged_nnz_lo += d.col[p] < mbeg;
                             if (!seen[d.col[p]]) {
                                 seen[d.col[p]] = 1;
                                 ++l.merged_nbr;
                                 l.merged_nbr_lo += d.col[p] < mbeg;
+                            }
+                            if (light && !seen_l[d.col[p]]) {
+                                seen_l[d.col[p]] = 1;
+                                ++l.merged_nbr_light;
                             }
                         }
                     }

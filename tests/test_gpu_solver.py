@@ -451,3 +451,43 @@ def test_device_validation_matches_host(rng, monkeypatch):
     two = sp.block_diag([L, L], format="csr")
     with pytest.raises(P.DomainError, match="not connected"):
         S._validate_laplacian(two)
+
+
+def test_segment_launch_forms_agree_bitwise():
+    """Hub rows: the sweep segments computed by a k_seg launch of their own
+    (with column windows and the bounded first sweep's leading-segment lists)
+    give bit for bit the solution of the in-kernel segment form."""
+    import hashlib
+    import os
+    import subprocess
+    import sys
+
+    code = r'''
+import hashlib, numpy as np
+import paper_1607_02955_b200 as P
+rng = np.random.default_rng(3)
+n = 4000
+hubs = np.arange(12)
+u = [np.arange(n - 1)]; v = [np.arange(1, n)]
+for hb in hubs:  # hubs of 700-3000 neighbours
+    nb = rng.choice(np.arange(12, n), size=700 + 200 * int(hb), replace=False)
+    u.append(np.full(nb.size, hb)); v.append(nb)
+u = np.concatenate(u); v = np.concatenate(v)
+keep = u != v
+g = P.Graph.from_edges(u[keep], v[keep], rng.random(int(keep.sum())) + 0.5, n=n)
+h = P.setup(P.laplacian(g), P.SolverConfig(tau=1e-9), stall_breaker=False)
+b = rng.standard_normal((40, n)); b -= b.mean(axis=1, keepdims=True)
+x = np.stack([p.values for p in P.solve_many(h, b)])
+assert max(p for p in [h.stats.max_residual]) <= 1e-9
+print("HASH", hashlib.sha256(x.tobytes()).hexdigest())
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for name, pre in (("own_launch", "1"), ("in_kernel", "1000000000")):
+        env = dict(os.environ, PYTHONPATH=root, CF_PRE_SEG_MIN=pre, CF_WIN_ROWS="256",
+                   CF_WIN_DEG="128")
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[name] = [ln for ln in r.stdout.splitlines() if ln.startswith("HASH")][0]
+    assert out["own_launch"] == out["in_kernel"]
