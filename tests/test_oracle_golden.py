@@ -103,3 +103,26 @@ def test_workload_graphs_match_product_generators():
     wl, bc = OW.make("c2"), configs.make("c2")
     assert np.array_equal(wl["graph"][1], bc.graph.indices)
     assert np.array_equal(wl["query"], bc.query)
+
+
+def test_rmat_goldens_are_wired():
+    """C4 / C5 fixtures (tests/golden/make_golden.py c4, make_golden_c5.py): the
+    values the -m gpu parity tests compare against are present, converged to
+    their tolerances and mutually consistent (the tau 1e-6 sums within 1e-6 of
+    the tau 1e-10 ones -- the reference's own accuracy at the config tau)."""
+    for name, rows, nq in (("config4.npz", 4, 1000), ("config5.npz", 8, 1)):
+        d = golden(name)
+        assert int(d["jl_rows"]) == rows and d["query"].size == nq
+        for tag, tau in (("1em06", 1e-6), ("1em10", 1e-10)):
+            assert d[f"jl_psum_{tag}"].shape == (nq,)
+            assert d[f"jl_res_{tag}"].shape == (rows,) and d[f"jl_res_{tag}"].max() <= tau
+        rel = np.abs(d["jl_psum_1em06"] / d["jl_psum_1em10"] - 1).max()
+        assert rel <= 1e-6, rel
+    d4, d5 = golden("config4.npz"), golden("config5.npz")
+    # C4 comes from the reference package itself (its stalled 3,576-level hierarchy)
+    assert (int(d4["n"]), int(d4["m"]), int(d4["k"])) == (646140, 15700710, 256)
+    assert d4["sizes"].size == 3576 and float(d4["t_setup"]) > 1000
+    # C5 from the oracle solve loop on this build's hierarchy (reference setup cannot finish)
+    assert (int(d5["n"]), int(d5["m"]), int(d5["k"])) == (2234040, 48492111, 650)
+    assert "oracle" in str(d5["source"]) and d5["samp_r_1em10"].shape == d5["samp_pivots"].shape
+    assert np.all(d5["samp_r_1em10"] > 0)
