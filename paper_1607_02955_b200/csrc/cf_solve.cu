@@ -802,8 +802,14 @@ __global__ void __launch_bounds__(kThreads, (KC > 128 ? 2 : CF_RED_CTAS)) k_elim
 // Partial sums of heavy-row segments: P[s] = sum over [sbeg[s], send[s]).
 // DEEP: launches with few segments (a handful per SM) are latency-bound, so
 // every warp keeps 4x the neighbour rows in flight (1 CTA/SM by registers).
-template <int KC, int MODE, bool DEEP = false>
-__global__ void __launch_bounds__(kThreads, DEEP ? 1 : (KC > 128 ? 2 : kGatherCtas)) k_seg(int64_t s_lo, int64_t s_hi,
+// MANY: launches of tens of thousands of CTAs (the hub levels of power-law
+// graphs) are bound by the L2 -> SM throughput, not by latency per warp: 4
+// CTAs/SM with half the rows in flight per warp (C5 sweep, ms per estimate:
+// 3 CTAs x 4 rows 1,454; 4 x 2 rows 1,399; 5 x 2 1,513; 6 x 1 1,497).  Levels
+// that fit the L2 (C2, C3) prefer 3 x 4 (C2 12.14 vs 11.53 ms with 4 x 2
+// everywhere), so only the large launches switch.
+template <int KC, int MODE, bool DEEP = false, bool MANY = false>
+__global__ void __launch_bounds__(kThreads, DEEP ? 1 : (KC > 128 ? 2 : (MANY ? 4 : kGatherCtas))) k_seg(int64_t s_lo, int64_t s_hi,
                                                   const int64_t* __restrict__ sbeg,
                                                   const int64_t* __restrict__ send,
                                                   const int32_t* __restrict__ col,
@@ -820,7 +826,8 @@ __global__ void __launch_bounds__(kThreads, DEEP ? 1 : (KC > 128 ? 2 : kGatherCt
     if (sord) sg = sord[sg];
     DV<V> acc;
     zero(acc);
-    gather_row<KC, MODE, DEEP ? 4 * CF_GATHER_DOUBLES : CF_GATHER_DOUBLES>(
+    gather_row<KC, MODE, DEEP ? 4 * CF_GATHER_DOUBLES
+                               : (MANY && KC <= 128) ? CF_GATHER_DOUBLES / 2 : CF_GATHER_DOUBLES>(
         col, val, sbeg[sg], send[sg], map, div, X, c0, acc, jlim);
     stv<V>(P + (size_t)sg * KC + c0, acc);
 }
@@ -1084,6 +1091,10 @@ static inline unsigned grid_rows(int64_t rows, int64_t at_least = 1) {
 #define CF_DEEP_SEG_CTAS 296
 #endif
 constexpr unsigned kDeepSegCtas = CF_DEEP_SEG_CTAS;  // <= 2 CTAs per SM: deep k_seg
+#ifndef CF_MANY_SEG_CTAS
+#define CF_MANY_SEG_CTAS 16384
+#endif
+constexpr unsigned kManySegCtas = CF_MANY_SEG_CTAS;  // L2-bound launches: 4 CTAs/SM k_seg
 static inline unsigned grid_tiles(int64_t rows, int64_t at_least = 1, int rpw = kTileRows / kWarps) {
     const int64_t t = (int64_t)kWarps * rpw;
     return (unsigned)std::max<int64_t>(at_least, (rows + t - 1) / t);
@@ -1183,6 +1194,10 @@ struct Ops {
             if (grid <= kDeepSegCtas)
                 launch_k(k_seg<KC, MODE, true>, dim3(grid), dim3(kThreads), 0, h.s, a, b, pl.sbeg,
                          pl.send, col, val, map, div, X, h.SP, (const int32_t*)pl.sord_lo, jlim);
+            else if (grid >= kManySegCtas)
+                launch_k(k_seg<KC, MODE, false, true>, dim3(grid), dim3(kThreads), 0, h.s, a, b,
+                         pl.sbeg, pl.send, col, val, map, div, X, h.SP,
+                         (const int32_t*)pl.sord_lo, jlim);
             else
                 launch_k(k_seg<KC, MODE, false>, dim3(grid), dim3(kThreads), 0, h.s, a, b, pl.sbeg,
                          pl.send, col, val, map, div, X, h.SP, (const int32_t*)pl.sord_lo, jlim);
@@ -1201,6 +1216,9 @@ struct Ops {
         if (grid <= kDeepSegCtas)
             launch_k(k_seg<KC, MODE, true>, dim3(grid), dim3(kThreads), 0, h.s, lo, hi, pl.sbeg,
                      pl.send, col, val, map, div, X, h.SP, ord, jlim);
+        else if (grid >= kManySegCtas)
+            launch_k(k_seg<KC, MODE, false, true>, dim3(grid), dim3(kThreads), 0, h.s, lo, hi,
+                     pl.sbeg, pl.send, col, val, map, div, X, h.SP, ord, jlim);
         else
             launch_k(k_seg<KC, MODE, false>, dim3(grid), dim3(kThreads), 0, h.s, lo, hi, pl.sbeg,
                      pl.send, col, val, map, div, X, h.SP, ord, jlim);
