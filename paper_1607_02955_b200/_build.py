@@ -23,7 +23,7 @@ OBJ = os.path.join(ROOT, "build", "obj")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + INC, "-I" + CSRC,
               "--expt-relaxed-constexpr"]
-SOURCES = ["cf_setup.cpp", "cf_solve.cu", "cf_estimators.cu", "cf_graph.cu", "cf_setup_dev.cu"]
+SOURCES = ["cf_setup.cpp", "cf_solve.cu", "cf_solve_hub.cu", "cf_estimators.cu", "cf_graph.cu", "cf_setup_dev.cu"]
 
 
 def _nvcc() -> str:
@@ -34,7 +34,8 @@ def _nvcc() -> str:
 
 
 def _deps(src: str) -> list[str]:
-    hdrs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
+    # cf_solve_hub.cu includes cf_solve.cu: every source counts as a dependency
+    hdrs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh", ".cu"))]
     return [os.path.join(CSRC, src), os.path.join(INC, "cfcent_b200.h"), *hdrs]
 
 

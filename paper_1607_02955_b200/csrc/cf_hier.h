@@ -157,6 +157,9 @@ struct Hier {
     long long* d_vcyc = nullptr;
     bool prof = false;
     bool host_loop = false;  // CF_HOST_LOOP=1
+    // power-law graph (level-0 maximum degree > 64 x mean on > 262,144 nodes):
+    // the solve runs the v_hub build of the kernels (cf_solve_hub.cu)
+    bool hub_profile = false;
     std::vector<ProfRec> recs;
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;

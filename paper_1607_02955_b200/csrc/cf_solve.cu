@@ -36,13 +36,28 @@
 #define CF_RED_CTAS 3  // min CTAs/SM for the reduction / restriction gather kernels
 #endif
 
+// The kernels and the solve driver live in a variant namespace: this file is
+// compiled twice, as itself (v_default: the launch bounds / rows-in-flight
+// measured best on graphs whose levels fit the L2) and through
+// cf_solve_hub.cu (v_hub: 4 CTAs/SM with half the rows in flight, measured
+// 3.6 % faster on the L2-bound hub levels of power-law graphs and 5 % slower
+// elsewhere; profiles/r02/occupancy_sweep_c5.txt).  Same arithmetic in both;
+// solve_block picks by Hier::hub_profile.
+#ifndef CF_VNS
+#define CF_VNS v_default
+#endif
+
 namespace cf {
 
+#ifndef CF_HUB_TU
 static thread_local std::string g_last_error;
 void set_error(const std::string& m) { g_last_error = m; }
+#endif
 
 // COL_KRYLOV: slowly converging column handed to V-cycle-preconditioned FCG
 enum ColState { COL_ZERO = 0, COL_ACTIVE = 1, COL_CONV = 2, COL_FALLBACK = 3, COL_KRYLOV = 4 };
+
+namespace CF_VNS {
 
 // ============================================================================
 // kernels
@@ -2077,6 +2092,34 @@ static void solve_block_t(Hier& h, int ncols, const CfSolveParams& p, double* re
     st.fallback_solves += fallback_cols;
 }
 
+#define CF_DISPATCH(KCV, ...)                        \
+    switch (KCV) {                                    \
+        case 1: { constexpr int K_ = 1; __VA_ARGS__; } break;     \
+        case 8: { constexpr int K_ = 8; __VA_ARGS__; } break;     \
+        case 16: { constexpr int K_ = 16; __VA_ARGS__; } break;   \
+        case 32: { constexpr int K_ = 32; __VA_ARGS__; } break;   \
+        case 64: { constexpr int K_ = 64; __VA_ARGS__; } break;   \
+        case 128: { constexpr int K_ = 128; __VA_ARGS__; } break; \
+        case 160: { constexpr int K_ = 160; __VA_ARGS__; } break; \
+        case 192: { constexpr int K_ = 192; __VA_ARGS__; } break; \
+        case 256: { constexpr int K_ = 256; __VA_ARGS__; } break; \
+        default: throw CfError(CF_RUNTIME, "unsupported block width"); \
+    }
+
+}  // namespace CF_VNS
+
+#ifdef CF_HUB_TU
+// hub-profile translation unit: only the block solve is exported
+void solve_block_hub(Hier& h, int kc, int ncols, const CfSolveParams& p, double* res_out,
+                     CfSolveStats& st) {
+    CF_DISPATCH(kc, CF_VNS::solve_block_t<K_>(h, ncols, p, res_out, st));
+}
+}  // namespace cf
+#else
+using namespace CF_VNS;
+void solve_block_hub(Hier& h, int kc, int ncols, const CfSolveParams& p, double* res_out,
+                     CfSolveStats& st);
+
 // Chunk width for the next `rem` columns.  Measured per-width block-solve
 // cost (tools/kc_cost.py, profiles/r01/kc_cost_*.txt): 256 columns cost more
 // than two chunks of 128 (the per-level X block of 256 columns leaves the L2),
@@ -2127,22 +2170,12 @@ static int kc_at_least(int k) {
     return 256;
 }
 
-#define CF_DISPATCH(KCV, ...)                        \
-    switch (KCV) {                                    \
-        case 1: { constexpr int K_ = 1; __VA_ARGS__; } break;     \
-        case 8: { constexpr int K_ = 8; __VA_ARGS__; } break;     \
-        case 16: { constexpr int K_ = 16; __VA_ARGS__; } break;   \
-        case 32: { constexpr int K_ = 32; __VA_ARGS__; } break;   \
-        case 64: { constexpr int K_ = 64; __VA_ARGS__; } break;   \
-        case 128: { constexpr int K_ = 128; __VA_ARGS__; } break; \
-        case 160: { constexpr int K_ = 160; __VA_ARGS__; } break; \
-        case 192: { constexpr int K_ = 192; __VA_ARGS__; } break; \
-        case 256: { constexpr int K_ = 256; __VA_ARGS__; } break; \
-        default: throw CfError(CF_RUNTIME, "unsupported block width"); \
-    }
-
 void solve_block(Hier& h, int kc, int ncols, const CfSolveParams& p, double* res_out,
                  CfSolveStats& st) {
+    if (h.hub_profile) {
+        solve_block_hub(h, kc, ncols, p, res_out, st);
+        return;
+    }
     CF_DISPATCH(kc, solve_block_t<K_>(h, ncols, p, res_out, st));
 }
 
@@ -2817,6 +2850,18 @@ extern "C" int cf_hier_create(int32_t nlev, const CfLevelDesc* ds, int32_t devic
                 if (d.coarse_op && d.n > 1) l.M = upload(*h, d.coarse_op, (size_t)d.n * d.n);
             }
         }
+        {
+            // kernel profile: power-law graphs (hub levels bound by the L2 -> SM
+            // throughput) run the v_hub build; CF_HUB_PROFILE=0/1 overrides
+            const CfLevelDesc& d0 = ds[0];
+            int64_t maxdeg = 0;
+            if (d0.rowptr)
+                for (int32_t i = 0; i < d0.n; ++i)
+                    maxdeg = std::max<int64_t>(maxdeg, d0.rowptr[i + 1] - d0.rowptr[i]);
+            const double mean = d0.n > 0 ? (double)d0.nnz_off / d0.n : 0.0;
+            h->hub_profile = d0.n > 262144 && (double)maxdeg > 64.0 * std::max(mean, 1.0);
+            if (const char* e = std::getenv("CF_HUB_PROFILE")) h->hub_profile = std::atoi(e) != 0;
+        }
         h->sums = (double*)h->dalloc(sizeof(double) * 8 * kMaxKC);
         h->coef = (double*)h->dalloc(sizeof(double) * 4 * kMaxKC);
         h->bn = (double*)h->dalloc(sizeof(double) * kMaxKC);
@@ -3060,3 +3105,4 @@ extern "C" int cf_hier_set_order(void* hp, const int32_t* perm, int64_t n) {
     CF_CUDA(cudaMemcpy(h.perm0, perm, sizeof(int32_t) * n, cudaMemcpyHostToDevice));
     CF_API_END
 }
+#endif  // CF_HUB_TU
