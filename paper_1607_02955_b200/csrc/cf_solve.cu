@@ -32,6 +32,9 @@
 // of spills in k_residual<128>), so it stays off.
 #define CF_HOIST_OWN 0
 #endif
+#ifndef CF_MANY_CTAS
+#define CF_MANY_CTAS 4  // CTAs/SM of the k_seg launches of >= CF_MANY_SEG_CTAS CTAs
+#endif
 #ifndef CF_RED_CTAS
 #define CF_RED_CTAS 3  // min CTAs/SM for the reduction / restriction gather kernels
 #endif
@@ -824,7 +827,7 @@ __global__ void __launch_bounds__(kThreads, (KC > 128 ? 2 : CF_RED_CTAS)) k_elim
 // that fit the L2 (C2, C3) prefer 3 x 4 (C2 12.14 vs 11.53 ms with 4 x 2
 // everywhere), so only the large launches switch.
 template <int KC, int MODE, bool DEEP = false, bool MANY = false>
-__global__ void __launch_bounds__(kThreads, DEEP ? 1 : (KC > 128 ? 2 : (MANY ? 4 : kGatherCtas))) k_seg(int64_t s_lo, int64_t s_hi,
+__global__ void __launch_bounds__(kThreads, DEEP ? 1 : (KC > 128 ? 2 : (MANY ? CF_MANY_CTAS : kGatherCtas))) k_seg(int64_t s_lo, int64_t s_hi,
                                                   const int64_t* __restrict__ sbeg,
                                                   const int64_t* __restrict__ send,
                                                   const int32_t* __restrict__ col,
